@@ -1,0 +1,163 @@
+/*
+ * lshbloom.h -- C-ABI of the B200-native LSHBloom hot path (arXiv 2411.04257).
+ *
+ * The library computes, for every document of a CSR batch of uint32 word ids:
+ *   word n-gram shingle fingerprints,
+ *   a num_perm-wide MinHash signature sig[i] = min_x ((a_i x + b_i) mod (2^61-1)) mod 2^32
+ *     (S:132-140),
+ *   b band hashes over r rows each, BH_j = (sum_u (c_u sig[j r + u] + d_u) mod P) mod P
+ *     (S:202-210),
+ *   a k-probe query-then-insert of each band hash into that band's own Bloom filter of
+ *     m = ceil(-n ln p / (ln 2)^2) bits, k = max(1, round((m/n) ln 2)) probes
+ *     (S:263),
+ *   and the duplicate flag = OR over bands ("If there is a collision for any band of
+ *     signatures, we mark that document as a duplicate").
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.  Every convention the paper
+ * leaves open (fingerprint, family PRNG, truncation order, probe derivation) is fixed in
+ * DESIGN.md section 3; outputs are bit-identical to the CPU oracle in oracle/.
+ *
+ * Conventions common to every entry point
+ * ---------------------------------------
+ *  - Return codes mirror SPEC's exit codes:
+ *      LSHBLOOM_OK 0, LSHBLOOM_EUSAGE 1 (bad argument / NULL pointer / malformed offsets),
+ *      LSHBLOOM_EDATA 2 (an empty document, S:64 -- the whole batch is rejected before any
+ *      filter is modified; lshbloom_last_error names the first bad index),
+ *      LSHBLOOM_ERUNTIME 3 (CUDA failure: the handle is poisoned and every later call
+ *      returns 3), LSHBLOOM_ENOMEM 4 (device allocation failed).
+ *  - Ownership: the caller owns every batch and output buffer; outputs live in the same
+ *    memory space as the batch (device memory of the handle's GPU when on_device = 1, host
+ *    memory otherwise; pinned host memory enables overlapped copies).  The library owns
+ *    filters, coefficients and scratch (cudaMalloc) and frees them in lshbloom_destroy.
+ *  - A handle is not thread-safe.  query_insert calls are serialised by the caller and
+ *    their order is the stream order.  Every call is complete (its stream
+ *    synchronised) when it returns.
+ *  - Outputs are pure functions of (parameters, seed, ordered concatenation of batches):
+ *    independent of batch boundaries, GPU count and launch configuration.
+ */
+#ifndef LSHBLOOM_H
+#define LSHBLOOM_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LSHBLOOM_API __attribute__((visibility("default")))
+#else
+#define LSHBLOOM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSHBLOOM_OK 0
+#define LSHBLOOM_EUSAGE 1
+#define LSHBLOOM_EDATA 2
+#define LSHBLOOM_ERUNTIME 3
+#define LSHBLOOM_ENOMEM 4
+
+#define LSHBLOOM_MAX_BANDS 64   /* bands per handle */
+#define LSHBLOOM_MAX_PERM 1024  /* num_perm */
+#define LSHBLOOM_MAX_K 64       /* probes per band hash (p >= ~5e-20) */
+
+typedef struct lshbloom lshbloom; /* opaque */
+
+/* A CSR batch.  Document d is tokens[offsets[d], offsets[d+1]).
+ *   n_docs    >= 1 and < 2^32
+ *   offsets   n_docs+1 entries, offsets[0] = 0, non-decreasing; an equal pair is an
+ *             empty document (error 2)
+ *   tokens    offsets[n_docs] word ids (any uint32 value, including 0)
+ *   on_device 1: offsets/tokens (and outputs) are device pointers on the handle's GPU;
+ *             0: host pointers (pinned preferred) -- host<->device copies are done inside
+ *   stream    cudaStream_t to run on (NULL: the handle's own stream) */
+typedef struct {
+    uint64_t n_docs;
+    const uint64_t *offsets;
+    const uint32_t *tokens;
+    int32_t on_device;
+    void *stream;
+} lshbloom_batch;
+
+/* Extended configuration (lshbloom_create fills shingle_n = 5, device = current,
+ * rank = 0, world = 1, sub_batch = 0 = default). */
+typedef struct {
+    uint32_t num_perm;   /* 1..LSHBLOOM_MAX_PERM */
+    uint32_t b;          /* bands, 1..LSHBLOOM_MAX_BANDS */
+    uint32_t r;          /* rows per band, b*r <= num_perm */
+    uint32_t shingle_n;  /* word n-gram width, >= 1 (DESIGN R2: 5) */
+    uint64_t n_expected; /* capacity n of every filter, >= 1 */
+    double fp_rate;      /* per-filter false-positive rate p in (0,1) (DESIGN R8) */
+    uint64_t seed;       /* hash-family seed (DESIGN R5) */
+    int32_t device;      /* CUDA device ordinal, -1 = current */
+    uint32_t rank;       /* band sharding: this rank owns bands [band_lo, band_hi) */
+    uint32_t world;      /*   over world ranks (bands split as evenly as possible) */
+    uint32_t sub_batch;  /* documents per Bloom sub-batch (0 = default 65536); results do
+                            not depend on it */
+} lshbloom_config;
+
+typedef struct {
+    uint64_t m;               /* bits per filter (analytic, the probe modulus) */
+    uint32_t k;               /* probes per band hash */
+    uint32_t num_perm, b, r, shingle_n;
+    uint32_t band_lo, band_hi;/* owned bands (global indices) */
+    uint64_t words_per_band;  /* uint32 words per filter = 2*ceil(m/64) */
+    uint64_t filter_bytes;    /* device bytes of the owned filters */
+    double p_eff;             /* 1-(1-p)^b */
+    uint64_t doc_count;       /* documents inserted so far */
+    int32_t oversubscribed;   /* doc_count > n_expected */
+    uint64_t seed;
+    uint64_t n_expected;
+    double fp_rate;
+} lshbloom_info_t;
+
+/* Create an index of b Bloom filters: sizes them from (n_expected, fp_rate),
+ * expands the hash family from seed and zeroes the filters.  shingle n = 5.
+ * On error *out is NULL and lshbloom_last_error(NULL) describes it. */
+LSHBLOOM_API int lshbloom_create(uint32_t num_perm, uint32_t b, uint32_t r, uint64_t n_expected,
+                    double fp_rate, uint64_t seed, lshbloom **out);
+LSHBLOOM_API int lshbloom_create_ex(const lshbloom_config *cfg, lshbloom **out);
+
+/* Release every resource; NULL-safe. */
+LSHBLOOM_API void lshbloom_destroy(lshbloom *h);
+
+/* MinHash signatures sig_out[n_docs][num_perm] (uint32, row-major).  Pure: no filter
+ * state is read or written.  Rows >= b*r are computed too. */
+LSHBLOOM_API int lshbloom_signatures(lshbloom *h, const lshbloom_batch *batch, uint32_t *sig_out);
+
+/* Band hashes bh_out[n_docs][b] (uint64, values < 2^61-1) for ALL b bands.  Pure. */
+LSHBLOOM_API int lshbloom_band_hashes(lshbloom *h, const lshbloom_batch *batch, uint64_t *bh_out);
+
+/* Query-then-insert every document of the batch in stream order against the owned band
+ * filters (all bands when world = 1): dup_out[d] = 1 iff some owned band's k probe bits
+ * were all set before document d (by earlier batches or earlier documents of this batch),
+ * else 0; then all band hashes are inserted (insert is unconditional).  Mutates the
+ * filters.  With world > 1 the flags cover only the owned bands (combine with a max over
+ * ranks; see lshbloom_query_insert_bands and paper_2411_04257_b200.sharded). */
+LSHBLOOM_API int lshbloom_query_insert(lshbloom *h, const lshbloom_batch *batch, uint8_t *dup_out);
+
+/* Bloom stage only, for band-sharded use: bh_owned[n_docs][band_hi-band_lo] holds the
+ * band hashes of the owned bands for n_docs documents in global stream order;
+ * hit_out[n_docs] = OR over the owned bands of the per-band verdicts.  Pointers are device
+ * pointers when on_device = 1, host otherwise.  Mutates the owned filters. */
+LSHBLOOM_API int lshbloom_query_insert_bands(lshbloom *h, const uint64_t *bh_owned, uint64_t n_docs,
+                                int32_t on_device, void *stream, uint8_t *hit_out);
+
+/* Zero every owned filter and the document count (as right after create). */
+LSHBLOOM_API int lshbloom_reset(lshbloom *h);
+
+/* Copy owned band (band_hi > j >= band_lo, global index j) filter words to host memory
+ * dst (words_per_band uint32 words; bit g of the filter = bit g&31 of word g>>5). */
+LSHBLOOM_API int lshbloom_filter_copy(lshbloom *h, uint32_t j, uint32_t *dst);
+
+/* Parameters and derived sizes. */
+LSHBLOOM_API int lshbloom_info(const lshbloom *h, lshbloom_info_t *out);
+
+/* Last error message of h (or of the last failed create when h is NULL). */
+LSHBLOOM_API const char *lshbloom_last_error(const lshbloom *h);
+
+/* Number of kernel launches the library issued since create (launch-count evidence). */
+LSHBLOOM_API uint64_t lshbloom_launch_count(const lshbloom *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSHBLOOM_H */

@@ -1,0 +1,227 @@
+"""ctypes binding of include/lshbloom.h -- argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of ``liblshbloom.so``; this module only
+converts torch tensors / numpy arrays into pointers and sizes, allocates outputs with torch
+(device memory, streams) and translates return codes into exceptions.  There is no CPU
+fallback: if the library is missing, importing this module fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblshbloom.so")
+
+OK, EUSAGE, EDATA, ERUNTIME, ENOMEM = 0, 1, 2, 3, 4
+
+
+class LSHBloomError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__("lshbloom error %d: %s" % (code, msg))
+        self.code = code
+
+
+class _Batch(ctypes.Structure):
+    _fields_ = [("n_docs", ctypes.c_uint64), ("offsets", ctypes.c_void_p),
+                ("tokens", ctypes.c_void_p), ("on_device", ctypes.c_int32),
+                ("stream", ctypes.c_void_p)]
+
+
+class _Config(ctypes.Structure):
+    _fields_ = [("num_perm", ctypes.c_uint32), ("b", ctypes.c_uint32), ("r", ctypes.c_uint32),
+                ("shingle_n", ctypes.c_uint32), ("n_expected", ctypes.c_uint64),
+                ("fp_rate", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("device", ctypes.c_int32), ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32),
+                ("sub_batch", ctypes.c_uint32)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_uint64), ("k", ctypes.c_uint32), ("num_perm", ctypes.c_uint32),
+                ("b", ctypes.c_uint32), ("r", ctypes.c_uint32), ("shingle_n", ctypes.c_uint32),
+                ("band_lo", ctypes.c_uint32), ("band_hi", ctypes.c_uint32),
+                ("words_per_band", ctypes.c_uint64), ("filter_bytes", ctypes.c_uint64),
+                ("p_eff", ctypes.c_double), ("doc_count", ctypes.c_uint64),
+                ("oversubscribed", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("n_expected", ctypes.c_uint64), ("fp_rate", ctypes.c_double)]
+
+
+EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloom_signatures",
+           "lshbloom_band_hashes", "lshbloom_query_insert", "lshbloom_query_insert_bands",
+           "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info", "lshbloom_last_error",
+           "lshbloom_launch_count")
+
+
+def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError("liblshbloom.so not built (%s); run `python -c 'import __graft_entry__ as g; "
+                          "g.build()'`" % path)
+    lib = ctypes.CDLL(path)
+    vp, u32, u64, i32 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+    lib.lshbloom_create.argtypes = [u32, u32, u32, u64, ctypes.c_double, u64, ctypes.POINTER(vp)]
+    lib.lshbloom_create_ex.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(vp)]
+    lib.lshbloom_destroy.argtypes = [vp]
+    lib.lshbloom_destroy.restype = None
+    for f in ("lshbloom_signatures", "lshbloom_band_hashes", "lshbloom_query_insert"):
+        getattr(lib, f).argtypes = [vp, ctypes.POINTER(_Batch), vp]
+    lib.lshbloom_query_insert_bands.argtypes = [vp, vp, u64, i32, vp, vp]
+    lib.lshbloom_reset.argtypes = [vp]
+    lib.lshbloom_filter_copy.argtypes = [vp, u32, vp]
+    lib.lshbloom_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    lib.lshbloom_last_error.argtypes = [vp]
+    lib.lshbloom_last_error.restype = ctypes.c_char_p
+    lib.lshbloom_launch_count.argtypes = [vp]
+    lib.lshbloom_launch_count.restype = u64
+    for f in EXPORTS:
+        if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count"):
+            getattr(lib, f).restype = ctypes.c_int
+    return lib
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _raw(x, kind: str):
+    """(pointer, on_device, keepalive) for a contiguous tensor / array of 4- or 8-byte ints."""
+    if _is_torch(x):
+        import torch
+        if not x.is_contiguous():
+            raise ValueError("%s must be contiguous" % kind)
+        return x.data_ptr(), (1 if x.is_cuda else 0), x
+    a = np.ascontiguousarray(x)
+    return a.ctypes.data, 0, a
+
+
+class LSHBloom:
+    """One LSHBloom index (b Bloom filters, one per band) on one GPU.
+
+    Inputs are CSR batches: ``offsets`` (n+1, int64/uint64) and ``tokens`` (uint32/int32 word
+    ids).  CUDA tensors run device-resident on torch's current stream; host arrays / CPU
+    tensors are copied in and out inside the call (pinned memory enables overlap)."""
+
+    def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
+                 *, shingle_n: int = 5, device: int | None = None, rank: int = 0, world: int = 1,
+                 sub_batch: int = 0):
+        self._lib = lib()
+        if device is None:
+            try:
+                import torch
+                device = torch.cuda.current_device() if torch.cuda.is_available() else -1
+            except Exception:
+                device = -1
+        cfg = _Config(num_perm, b, r, shingle_n, n_expected, fp_rate, seed & (2**64 - 1), device,
+                      rank, world, sub_batch)
+        h = ctypes.c_void_p()
+        rc = self._lib.lshbloom_create_ex(ctypes.byref(cfg), ctypes.byref(h))
+        if rc:
+            raise LSHBloomError(rc, self._lib.lshbloom_last_error(None).decode())
+        self._h = h
+        self.num_perm, self.b, self.r = num_perm, b, r
+        self.device = device
+        inf = self.info()
+        self.m, self.k = inf["m"], inf["k"]
+        self.band_lo, self.band_hi = inf["band_lo"], inf["band_hi"]
+
+    # ------------------------------------------------------------------ plumbing
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._lib.lshbloom_destroy(h)
+
+    __del__ = close
+
+    def _check(self, rc: int):
+        if rc:
+            raise LSHBloomError(rc, self._lib.lshbloom_last_error(self._h).decode())
+
+    def _batch(self, offsets, tokens, stream):
+        po, do, ko = _raw(offsets, "offsets")
+        pt, dt, kt = _raw(tokens, "tokens")
+        if do != dt:
+            raise ValueError("offsets and tokens must live in the same memory space")
+        n = (offsets.numel() if _is_torch(offsets) else len(ko)) - 1
+        if stream is None and do:
+            import torch
+            stream = torch.cuda.current_stream(offsets.device).cuda_stream
+        return _Batch(n, po, pt, do, stream or None), (ko, kt), n, bool(do)
+
+    def _out(self, shape, np_dtype, torch_dtype, on_device, like):
+        if on_device:
+            import torch
+            return torch.empty(shape, dtype=torch_dtype, device=like.device)
+        return np.empty(shape, dtype=np_dtype)
+
+    @staticmethod
+    def _ptr(x):
+        return x.data_ptr() if _is_torch(x) else x.ctypes.data
+
+    # ------------------------------------------------------------------ the C-ABI calls
+    def signatures(self, offsets, tokens, *, stream=None):
+        """MinHash signatures [n][num_perm] uint32 (int32 when on the GPU)."""
+        import_torch_dtype = _torch_dtype("int32")
+        bt, keep, n, dev = self._batch(offsets, tokens, stream)
+        out = self._out((n, self.num_perm), np.uint32, import_torch_dtype, dev, offsets)
+        self._check(self._lib.lshbloom_signatures(self._h, ctypes.byref(bt), self._ptr(out)))
+        return out
+
+    def band_hashes(self, offsets, tokens, *, stream=None):
+        """Band hashes [n][b] uint64 (int64 when on the GPU) for all bands."""
+        bt, keep, n, dev = self._batch(offsets, tokens, stream)
+        out = self._out((n, self.b), np.uint64, _torch_dtype("int64"), dev, offsets)
+        self._check(self._lib.lshbloom_band_hashes(self._h, ctypes.byref(bt), self._ptr(out)))
+        return out
+
+    def query_insert(self, offsets, tokens, *, out=None, stream=None):
+        """Duplicate flags [n] uint8, stream order; mutates the filters."""
+        bt, keep, n, dev = self._batch(offsets, tokens, stream)
+        if out is None:
+            out = self._out((n,), np.uint8, _torch_dtype("uint8"), dev, offsets)
+        self._check(self._lib.lshbloom_query_insert(self._h, ctypes.byref(bt), self._ptr(out)))
+        return out
+
+    def query_insert_bands(self, bh_owned, *, out=None, stream=None):
+        """Bloom stage only: bh_owned [n][band_hi-band_lo] -> hit flags [n] (OR over owned bands)."""
+        p, dev, keep = _raw(bh_owned, "bh_owned")
+        n = bh_owned.shape[0]
+        if out is None:
+            out = self._out((n,), np.uint8, _torch_dtype("uint8"), dev, bh_owned)
+        if stream is None and dev:
+            import torch
+            stream = torch.cuda.current_stream(bh_owned.device).cuda_stream
+        self._check(self._lib.lshbloom_query_insert_bands(self._h, p, n, dev, stream or None,
+                                                          self._ptr(out)))
+        return out
+
+    def reset(self):
+        self._check(self._lib.lshbloom_reset(self._h))
+
+    def filter_words(self, j: int) -> np.ndarray:
+        out = np.empty(self.info()["words_per_band"], np.uint32)
+        self._check(self._lib.lshbloom_filter_copy(self._h, j, out.ctypes.data))
+        return out
+
+    def info(self) -> dict:
+        inf = _Info()
+        self._check(self._lib.lshbloom_info(self._h, ctypes.byref(inf)))
+        return {f: getattr(inf, f) for f, _ in _Info._fields_}
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.lshbloom_launch_count(self._h))
+
+
+def _torch_dtype(name: str):
+    import torch
+    return getattr(torch, name)

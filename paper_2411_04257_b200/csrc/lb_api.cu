@@ -1,0 +1,602 @@
+// lb_api.cu -- the C-ABI of include/lshbloom.h: handle, sizing, hash-family expansion, batch
+// staging (pinned host -> HBM, double-buffered against K1), and the per-call kernel sequence.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lshbloom.h"
+#include "lb_internal.h"
+
+using namespace lb;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+cudaError_t ensure(DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t c = bytes + bytes / 4 + 256;
+  cudaError_t e = cudaMalloc(&b.p, c);
+  if (e == cudaSuccess) b.cap = c;
+  return e;
+}
+
+thread_local std::string g_create_error;
+
+constexpr uint32_t kDefaultSubBatch = 65536;
+constexpr uint64_t kChunkTokens = 16ull << 20;   // host-batch staging chunk (64 MB of tokens)
+constexpr uint64_t kGenMax = (1ull << 22) - 1;
+
+// Counter-mode expansion R(seed, dom, i) (DESIGN R5).
+uint64_t R(uint64_t seed, uint64_t dom, uint64_t i) { return mix64(seed + kGamma * ((dom << 32) + i + 1)); }
+
+}  // namespace
+
+struct lshbloom {
+  lshbloom_config cfg{};
+  uint64_t m = 0, m_inv = 0, W = 0;
+  uint32_t k = 0, band_lo = 0, band_hi = 0, bl = 0, npl = 0, sub_batch = 0;
+  int device = 0, sm_count = 148;
+  cudaStream_t own_stream = nullptr, copy_stream = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_k1[2] = {nullptr, nullptr};
+  PermCoef* d_coef = nullptr;
+  uint64_t* d_bcoef = nullptr;
+  uint64_t* d_s1 = nullptr;
+  uint64_t* d_s2 = nullptr;
+  uint32_t* d_F = nullptr;
+  uint32_t* d_T2 = nullptr;
+  uint64_t* d_ekey = nullptr;
+  uint64_t* d_eval = nullptr;
+  uint32_t ecap_log2 = 0;
+  uint64_t gen = 1;
+  uint64_t* d_st = nullptr;       // 4 * sub_batch * bl
+  uint32_t* d_cand = nullptr;     // sub_batch * bl
+  uint32_t* d_counters = nullptr; // [0] candidates, [1..2] K1 work counters
+  ErrState* d_err = nullptr;
+  DevBuf off, tok[2], bh, dup, sig;
+  uint64_t doc_count = 0, launches = 0;
+  std::string err;
+  bool poisoned = false;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int fail(lshbloom* h, int code, const std::string& msg) {
+  if (h) h->err = msg;
+  else g_create_error = msg;
+  return code;
+}
+
+int fail_cuda(lshbloom* h, cudaError_t e, const char* what) {
+  std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(h, LSHBLOOM_ENOMEM, msg);
+  }
+  if (h) h->poisoned = true;
+  return fail(h, LSHBLOOM_ERUNTIME, msg);
+}
+
+#define LB_CUDA(h, call)                                 \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return fail_cuda(h, e_, #call); \
+  } while (0)
+
+int check_handle(lshbloom* h) {
+  if (!h) return fail(nullptr, LSHBLOOM_EUSAGE, "NULL handle");
+  if (h->poisoned) return fail(h, LSHBLOOM_ERUNTIME, "handle poisoned by an earlier CUDA error: " + h->err);
+  return LSHBLOOM_OK;
+}
+
+void free_all(lshbloom* h) {
+  auto F = [](void* p) { if (p) cudaFree(p); };
+  F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_T2); F(h->d_ekey);
+  F(h->d_eval); F(h->d_st); F(h->d_cand); F(h->d_counters); F(h->d_err);
+  F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p);
+  for (int i = 0; i < 2; i++) {
+    if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
+    if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
+  }
+  if (h->own_stream) cudaStreamDestroy(h->own_stream);
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+}
+
+// Host-side CSR validation; returns 0, 1 (usage) or 2 (empty doc).
+int validate_host(lshbloom* h, const uint64_t* off, uint64_t n) {
+  if (off[0] != 0) return fail(h, LSHBLOOM_EUSAGE, "offsets[0] must be 0");
+  for (uint64_t i = 0; i < n; i++) {
+    if (off[i + 1] < off[i]) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease at index " + std::to_string(i));
+    if (off[i + 1] == off[i])
+      return fail(h, LSHBLOOM_EDATA, "empty document at index " + std::to_string(i));
+  }
+  return LSHBLOOM_OK;
+}
+
+int check_batch(lshbloom* h, const lshbloom_batch* b) {
+  if (!b || !b->offsets || !b->tokens) return fail(h, LSHBLOOM_EUSAGE, "NULL batch / offsets / tokens");
+  if (b->n_docs == 0 || b->n_docs > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_docs must be in [1, 2^32)");
+  return LSHBLOOM_OK;
+}
+
+BandMap owned_map(const lshbloom* h) {
+  BandMap m;
+  memset(&m, 0, sizeof m);
+  for (uint32_t j = h->band_lo; j < h->band_hi; j++) {
+    m.ncol[j] = h->bl;
+    m.col[j] = j - h->band_lo;
+  }
+  return m;
+}
+
+BandMap full_map(const lshbloom* h) {
+  BandMap m;
+  memset(&m, 0, sizeof m);
+  for (uint32_t j = 0; j < h->cfg.b; j++) {
+    m.ncol[j] = h->cfg.b;
+    m.col[j] = j;
+  }
+  return m;
+}
+
+// Reset the error gate: flags = 0, gate = 0, first_empty = ~0.
+int reset_err(lshbloom* h, cudaStream_t s) {
+  LB_CUDA(h, cudaMemsetAsync(h->d_err, 0, 8, s));
+  LB_CUDA(h, cudaMemsetAsync(&h->d_err->first_empty, 0xFF, 8, s));
+  return LSHBLOOM_OK;
+}
+
+// After the stream is synchronised: translate the device validation result.
+int read_err(lshbloom* h) {
+  ErrState e;
+  LB_CUDA(h, cudaMemcpy(&e, h->d_err, sizeof e, cudaMemcpyDeviceToHost));
+  if (e.flags) return fail(h, LSHBLOOM_EUSAGE, "malformed offsets (offsets[0] != 0 or decreasing)");
+  if (e.first_empty != ~0ull)
+    return fail(h, LSHBLOOM_EDATA, "empty document at index " + std::to_string(e.first_empty));
+  return LSHBLOOM_OK;
+}
+
+MinhashParams base_params(lshbloom* h) {
+  MinhashParams p;
+  memset(&p, 0, sizeof p);
+  p.shingle_n = h->cfg.shingle_n;
+  p.fp_init_n = mix64(kFpSalt + h->cfg.shingle_n);
+  p.coef = h->d_coef;
+  p.num_perm = h->cfg.num_perm;
+  p.b = h->cfg.b;
+  p.r = h->cfg.r;
+  p.bcoef = h->d_bcoef;
+  p.err = &h->d_err->pad;
+  return p;
+}
+
+// K0 + K1 over a batch.  sig_dev / bh_dev are device outputs (either may be null).
+int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* sig_dev,
+                uint64_t* bh_dev, const BandMap& map) {
+  const uint64_t n = b->n_docs;
+  MinhashParams p = base_params(h);
+  p.sig_out = sig_dev;
+  p.bh_out = bh_dev;
+  p.map = map;
+  int rc = reset_err(h, s);
+  if (rc) return rc;
+  if (b->on_device) {
+    h->launches += launch_validate(b->offsets, n, h->d_err, s);
+    p.offsets = b->offsets;
+    p.tokens = b->tokens;
+    p.tok_base = 0;
+    p.doc0 = 0;
+    p.n_docs = (uint32_t)n;
+    p.counter = h->d_counters + 1;
+    LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s);
+    if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
+    h->launches += l;
+    LB_CUDA(h, cudaGetLastError());
+    return LSHBLOOM_OK;
+  }
+  // host batch: validate here, then stream token chunks through two staging buffers
+  rc = validate_host(h, b->offsets, n);
+  if (rc) return rc;
+  LB_CUDA(h, ensure(h->off, (n + 1) * sizeof(uint64_t)));
+  LB_CUDA(h, cudaMemcpyAsync(h->off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+  uint64_t maxdoc = 0;
+  for (uint64_t i = 0; i < n; i++) maxdoc = std::max(maxdoc, b->offsets[i + 1] - b->offsets[i]);
+  const uint64_t chunk = std::max(kChunkTokens, maxdoc);
+  const uint64_t total = b->offsets[n];
+  const uint64_t buf_tokens = std::min(chunk, total);
+  for (int i = 0; i < 2; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
+  p.offsets = (const uint64_t*)h->off.p;
+  uint64_t d0 = 0;
+  int c = 0;
+  while (d0 < n) {
+    // largest d1 with tokens [off[d0], off[d1]) <= chunk (at least one document)
+    const uint64_t t0 = b->offsets[d0];
+    const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk);
+    uint64_t d1 = (uint64_t)(lim - b->offsets) - 1;
+    if (d1 <= d0) d1 = d0 + 1;
+    const uint64_t t1 = b->offsets[d1];
+    const int buf = c & 1;
+    LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
+    LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, h->copy_stream));
+    LB_CUDA(h, cudaEventRecord(h->ev_h2d[buf], h->copy_stream));
+    LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_h2d[buf], 0));
+    p.tokens = (const uint32_t*)h->tok[buf].p;
+    p.tok_base = t0;
+    p.doc0 = (uint32_t)d0;
+    p.n_docs = (uint32_t)(d1 - d0);
+    p.counter = h->d_counters + 1 + buf;
+    LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s);
+    if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
+    h->launches += l;
+    LB_CUDA(h, cudaGetLastError());
+    LB_CUDA(h, cudaEventRecord(h->ev_k1[buf], s));
+    d0 = d1;
+    c++;
+  }
+  return LSHBLOOM_OK;
+}
+
+// K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
+int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t n, uint8_t* dup_dev, cudaStream_t s) {
+  BloomParams p;
+  memset(&p, 0, sizeof p);
+  p.F = h->d_F;
+  p.T2 = h->d_T2;
+  p.W = h->W;
+  p.m = h->m;
+  p.m_inv = h->m_inv;
+  p.k = h->k;
+  p.bl = h->bl;
+  p.s1 = h->d_s1;
+  p.s2 = h->d_s2;
+  p.ekey = h->d_ekey;
+  p.eval = h->d_eval;
+  p.ecap_log2 = h->ecap_log2;
+  p.bh = bh_dev;
+  const uint64_t SB = h->sub_batch;
+  p.st_g0 = h->d_st;
+  p.st_d = h->d_st + SB * h->bl;
+  p.st_pre = h->d_st + 2 * SB * h->bl;
+  p.st_arr = h->d_st + 3 * SB * h->bl;
+  p.cand = h->d_cand;
+  p.cand_count = h->d_counters;
+  p.dup = dup_dev;
+  p.err = &h->d_err->pad;
+  for (uint64_t i0 = 0; i0 < n; i0 += SB) {
+    if (h->gen >= kGenMax) {   // generation tags exhausted: clear E once every ~4M sub-batches
+      const uint64_t cap = 1ull << h->ecap_log2;
+      LB_CUDA(h, cudaMemsetAsync(h->d_ekey, 0, cap * 8, s));
+      LB_CUDA(h, cudaMemsetAsync(h->d_eval, 0, cap * 8, s));
+      h->gen = 1;
+    }
+    p.gen = h->gen++;
+    p.i0 = (uint32_t)i0;
+    p.nsb = (uint32_t)std::min<uint64_t>(SB, n - i0);
+    h->launches += launch_bloom_subbatch(p, h->sm_count, s);
+    LB_CUDA(h, cudaGetLastError());
+  }
+  return LSHBLOOM_OK;
+}
+
+int finish(lshbloom* h, cudaStream_t s) {
+  LB_CUDA(h, cudaStreamSynchronize(s));
+  LB_CUDA(h, cudaGetLastError());
+  return read_err(h);
+}
+
+}  // namespace
+
+extern "C" {
+
+int lshbloom_create(uint32_t num_perm, uint32_t b, uint32_t r, uint64_t n_expected, double fp_rate,
+                    uint64_t seed, lshbloom** out) {
+  lshbloom_config c;
+  memset(&c, 0, sizeof c);
+  c.num_perm = num_perm;
+  c.b = b;
+  c.r = r;
+  c.shingle_n = 5;
+  c.n_expected = n_expected;
+  c.fp_rate = fp_rate;
+  c.seed = seed;
+  c.device = -1;
+  c.rank = 0;
+  c.world = 1;
+  c.sub_batch = 0;
+  return lshbloom_create_ex(&c, out);
+}
+
+int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
+  if (!out) return fail(nullptr, LSHBLOOM_EUSAGE, "NULL out");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, LSHBLOOM_EUSAGE, "NULL config");
+  lshbloom_config c = *cfg;
+  if (c.num_perm == 0 || c.num_perm > LSHBLOOM_MAX_PERM) return fail(nullptr, LSHBLOOM_EUSAGE, "num_perm must be in [1, 1024]");
+  if (c.b == 0 || c.b > LSHBLOOM_MAX_BANDS) return fail(nullptr, LSHBLOOM_EUSAGE, "b must be in [1, 64]");
+  if (c.r == 0 || (uint64_t)c.b * c.r > c.num_perm) return fail(nullptr, LSHBLOOM_EUSAGE, "need r >= 1 and b*r <= num_perm (S:183)");
+  if (c.shingle_n == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "shingle_n must be >= 1");
+  if (c.n_expected == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "n_expected must be >= 1");
+  if (!(c.fp_rate > 0.0 && c.fp_rate < 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "fp_rate must be in (0, 1) (S:273)");
+  if (c.world == 0) c.world = 1;
+  if (c.rank >= c.world) return fail(nullptr, LSHBLOOM_EUSAGE, "rank must be < world");
+  if (c.world > c.b) return fail(nullptr, LSHBLOOM_EUSAGE, "world must be <= b (every rank owns >= 1 band)");
+
+  // Sizing, P:224-225 / S:263 (DESIGN R9): natural log, ceil for m, llround for k.
+  const double md = ceil(-(double)c.n_expected * log(c.fp_rate) / (log(2.0) * log(2.0)));
+  if (!(md >= 1.0) || md > 68719476736.0) return fail(nullptr, LSHBLOOM_EUSAGE, "filter size m must be <= 2^36 bits");
+  long long kk = llround((md / (double)c.n_expected) * log(2.0));
+  if (kk < 1) kk = 1;
+  if (kk > LSHBLOOM_MAX_K) return fail(nullptr, LSHBLOOM_EUSAGE, "k > 64 probes (fp_rate too small)");
+
+  lshbloom* h = new lshbloom();
+  h->cfg = c;
+  h->m = (uint64_t)md;
+  h->k = (uint32_t)kk;
+  h->m_inv = ~0ull / h->m;
+  h->W = 2 * ((h->m + 63) / 64);
+  const uint32_t base = c.b / c.world, rem = c.b % c.world;
+  h->band_lo = c.rank * base + std::min(c.rank, rem);
+  h->bl = base + (c.rank < rem ? 1 : 0);
+  h->band_hi = h->band_lo + h->bl;
+  uint32_t npl = 1;
+  while (npl * 32 < c.num_perm) npl *= 2;
+  h->npl = npl;
+  h->sub_batch = c.sub_batch ? c.sub_batch : kDefaultSubBatch;
+
+  int dev = c.device;
+  if (dev < 0) cudaGetDevice(&dev);
+  h->device = dev;
+  h->cfg.device = dev;
+  DeviceGuard guard(dev);
+  cudaError_t e;
+#define CR(call)                                     \
+  do {                                               \
+    e = (call);                                      \
+    if (e != cudaSuccess) {                          \
+      int rc_ = fail_cuda(nullptr, e, #call);        \
+      free_all(h);                                   \
+      delete h;                                      \
+      return rc_;                                    \
+    }                                                \
+  } while (0)
+  CR(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev));
+  CR(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+  CR(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; i++) {
+    CR(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming));
+    CR(cudaEventCreateWithFlags(&h->ev_k1[i], cudaEventDisableTiming));
+    CR(cudaEventRecord(h->ev_k1[i], h->own_stream));
+  }
+
+  // Hash family (DESIGN R5), in the kernel's limb layout.
+  std::vector<PermCoef> coef(32 * npl);
+  for (uint32_t i = 0; i < 32 * npl; i++) {
+    uint64_t a = 1, bb = 0;
+    if (i < c.num_perm) {
+      a = 1 + R(c.seed, 1, 2ull * i) % (kP - 1);
+      bb = R(c.seed, 1, 2ull * i + 1) % kP;
+    }
+    const uint64_t bp = bb + 1;
+    coef[i].a0 = (uint32_t)(a & 0x7FFFFFFFull);
+    coef[i].a1 = (uint32_t)(a >> 31);
+    coef[i].bp0 = (uint32_t)bp;
+    coef[i].bp1 = (uint32_t)(bp >> 32);
+  }
+  std::vector<uint64_t> bcoef(2 * c.r);
+  for (uint32_t u = 0; u < c.r; u++) {
+    bcoef[u] = 1 + R(c.seed, 2, 2ull * u) % (kP - 1);
+    bcoef[c.r + u] = R(c.seed, 2, 2ull * u + 1) % kP;
+  }
+  std::vector<uint64_t> s1(h->bl), s2(h->bl);
+  for (uint32_t jl = 0; jl < h->bl; jl++) {
+    s1[jl] = R(c.seed, 3, h->band_lo + jl);
+    s2[jl] = R(c.seed, 4, h->band_lo + jl);
+  }
+  CR(cudaMalloc(&h->d_coef, coef.size() * sizeof(PermCoef)));
+  CR(cudaMemcpy(h->d_coef, coef.data(), coef.size() * sizeof(PermCoef), cudaMemcpyHostToDevice));
+  CR(cudaMalloc(&h->d_bcoef, bcoef.size() * 8));
+  CR(cudaMemcpy(h->d_bcoef, bcoef.data(), bcoef.size() * 8, cudaMemcpyHostToDevice));
+  CR(cudaMalloc(&h->d_s1, h->bl * 8));
+  CR(cudaMalloc(&h->d_s2, h->bl * 8));
+  CR(cudaMemcpy(h->d_s1, s1.data(), h->bl * 8, cudaMemcpyHostToDevice));
+  CR(cudaMemcpy(h->d_s2, s2.data(), h->bl * 8, cudaMemcpyHostToDevice));
+
+  // Filters "with all bits initially set to 0" and the contested-mark bitmap.
+  const size_t fbytes = (size_t)h->bl * h->W * 4;
+  CR(cudaMalloc(&h->d_F, fbytes));
+  CR(cudaMemset(h->d_F, 0, fbytes));
+  CR(cudaMalloc(&h->d_T2, fbytes));
+  CR(cudaMemset(h->d_T2, 0, fbytes));
+
+  // Earliest-setter table: >= 2x the most contested positions a sub-batch can produce
+  // (each contested position has >= 2 of the sub_batch * bl * k probes).
+  const uint64_t probes = (uint64_t)h->sub_batch * h->bl * h->k;
+  uint32_t lg = 10;
+  while ((1ull << lg) < probes) lg++;
+  h->ecap_log2 = lg;
+  CR(cudaMalloc(&h->d_ekey, (8ull << lg)));
+  CR(cudaMalloc(&h->d_eval, (8ull << lg)));
+  CR(cudaMemset(h->d_ekey, 0, (8ull << lg)));
+  CR(cudaMemset(h->d_eval, 0, (8ull << lg)));
+  CR(cudaMalloc(&h->d_st, 4ull * h->sub_batch * h->bl * 8));
+  CR(cudaMalloc(&h->d_cand, (size_t)h->sub_batch * h->bl * 4));
+  CR(cudaMalloc(&h->d_counters, 16 * 4));
+  CR(cudaMemset(h->d_counters, 0, 16 * 4));
+  CR(cudaMalloc(&h->d_err, sizeof(ErrState)));
+  CR(cudaMemset(h->d_err, 0, sizeof(ErrState)));
+  CR(cudaDeviceSynchronize());
+#undef CR
+  *out = h;
+  return LSHBLOOM_OK;
+}
+
+void lshbloom_destroy(lshbloom* h) {
+  if (!h) return;
+  {
+    DeviceGuard g(h->device);
+    if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+    free_all(h);
+  }
+  delete h;
+}
+
+int lshbloom_signatures(lshbloom* h, const lshbloom_batch* b, uint32_t* sig_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if ((rc = check_batch(h, b))) return rc;
+  if (!sig_out) return fail(h, LSHBLOOM_EUSAGE, "NULL sig_out");
+  DeviceGuard g(h->device);
+  cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
+  const size_t bytes = b->n_docs * h->cfg.num_perm * sizeof(uint32_t);
+  uint32_t* dsig = sig_out;
+  if (!b->on_device) {
+    LB_CUDA(h, ensure(h->sig, bytes));
+    dsig = (uint32_t*)h->sig.p;
+  }
+  BandMap none;
+  memset(&none, 0, sizeof none);
+  if ((rc = run_minhash(h, b, s, dsig, nullptr, none))) return rc;
+  if (!b->on_device) LB_CUDA(h, cudaMemcpyAsync(sig_out, dsig, bytes, cudaMemcpyDeviceToHost, s));
+  return finish(h, s);
+}
+
+int lshbloom_band_hashes(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if ((rc = check_batch(h, b))) return rc;
+  if (!bh_out) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_out");
+  DeviceGuard g(h->device);
+  cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
+  const size_t bytes = b->n_docs * h->cfg.b * sizeof(uint64_t);
+  uint64_t* dbh = bh_out;
+  if (!b->on_device) {
+    LB_CUDA(h, ensure(h->bh, bytes));
+    dbh = (uint64_t*)h->bh.p;
+  }
+  if ((rc = run_minhash(h, b, s, nullptr, dbh, full_map(h)))) return rc;
+  if (!b->on_device) LB_CUDA(h, cudaMemcpyAsync(bh_out, dbh, bytes, cudaMemcpyDeviceToHost, s));
+  return finish(h, s);
+}
+
+int lshbloom_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if ((rc = check_batch(h, b))) return rc;
+  if (!dup_out) return fail(h, LSHBLOOM_EUSAGE, "NULL dup_out");
+  DeviceGuard g(h->device);
+  cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
+  const uint64_t n = b->n_docs;
+  LB_CUDA(h, ensure(h->bh, n * h->bl * sizeof(uint64_t)));
+  uint8_t* ddup = dup_out;
+  if (!b->on_device) {
+    LB_CUDA(h, ensure(h->dup, n));
+    ddup = (uint8_t*)h->dup.p;
+  }
+  if ((rc = run_minhash(h, b, s, nullptr, (uint64_t*)h->bh.p, owned_map(h)))) return rc;
+  LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, s));
+  if ((rc = run_bloom(h, (const uint64_t*)h->bh.p, n, ddup, s))) return rc;
+  if (!b->on_device) LB_CUDA(h, cudaMemcpyAsync(dup_out, ddup, n, cudaMemcpyDeviceToHost, s));
+  if ((rc = finish(h, s))) return rc;
+  h->doc_count += n;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t n_docs, int32_t on_device,
+                                void* stream, uint8_t* hit_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!bh_owned || !hit_out) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_owned / hit_out");
+  if (n_docs == 0 || n_docs > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_docs must be in [1, 2^32)");
+  DeviceGuard g(h->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
+  const size_t bytes = n_docs * h->bl * sizeof(uint64_t);
+  const uint64_t* dbh = bh_owned;
+  uint8_t* dhit = hit_out;
+  if (!on_device) {
+    LB_CUDA(h, ensure(h->bh, bytes));
+    LB_CUDA(h, ensure(h->dup, n_docs));
+    LB_CUDA(h, cudaMemcpyAsync(h->bh.p, bh_owned, bytes, cudaMemcpyHostToDevice, s));
+    dbh = (const uint64_t*)h->bh.p;
+    dhit = (uint8_t*)h->dup.p;
+  }
+  if ((rc = reset_err(h, s))) return rc;
+  LB_CUDA(h, cudaMemsetAsync(dhit, 0, n_docs, s));
+  if ((rc = run_bloom(h, dbh, n_docs, dhit, s))) return rc;
+  if (!on_device) LB_CUDA(h, cudaMemcpyAsync(hit_out, dhit, n_docs, cudaMemcpyDeviceToHost, s));
+  if ((rc = finish(h, s))) return rc;
+  h->doc_count += n_docs;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_reset(lshbloom* h) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  DeviceGuard g(h->device);
+  LB_CUDA(h, cudaMemsetAsync(h->d_F, 0, (size_t)h->bl * h->W * 4, h->own_stream));
+  LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
+  h->doc_count = 0;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_filter_copy(lshbloom* h, uint32_t j, uint32_t* dst) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!dst || j < h->band_lo || j >= h->band_hi) return fail(h, LSHBLOOM_EUSAGE, "band not owned by this handle / NULL dst");
+  DeviceGuard g(h->device);
+  LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
+  LB_CUDA(h, cudaMemcpy(dst, h->d_F + (uint64_t)(j - h->band_lo) * h->W, h->W * 4, cudaMemcpyDeviceToHost));
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_info(const lshbloom* h, lshbloom_info_t* out) {
+  if (!h || !out) return LSHBLOOM_EUSAGE;
+  memset(out, 0, sizeof *out);
+  out->m = h->m;
+  out->k = h->k;
+  out->num_perm = h->cfg.num_perm;
+  out->b = h->cfg.b;
+  out->r = h->cfg.r;
+  out->shingle_n = h->cfg.shingle_n;
+  out->band_lo = h->band_lo;
+  out->band_hi = h->band_hi;
+  out->words_per_band = h->W;
+  out->filter_bytes = (uint64_t)h->bl * h->W * 4;
+  out->p_eff = -expm1((double)h->cfg.b * log1p(-h->cfg.fp_rate));   // 1-(1-p)^b
+  out->doc_count = h->doc_count;
+  out->oversubscribed = h->doc_count > h->cfg.n_expected ? 1 : 0;
+  out->seed = h->cfg.seed;
+  out->n_expected = h->cfg.n_expected;
+  out->fp_rate = h->cfg.fp_rate;
+  return LSHBLOOM_OK;
+}
+
+const char* lshbloom_last_error(const lshbloom* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+uint64_t lshbloom_launch_count(const lshbloom* h) { return h ? h->launches : 0; }
+
+}  // extern "C"

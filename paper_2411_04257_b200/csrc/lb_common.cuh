@@ -1,0 +1,57 @@
+// lb_common.cuh -- device/host helpers of the CUDA path (sm_100a).
+//
+// Independent implementation of the conventions in DESIGN.md section 3; shares no code
+// with oracle/ (the CPU oracle re-implements every step for parity testing).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lb {
+
+constexpr uint64_t kP = 0x1FFFFFFFFFFFFFFFull;   // 2^61 - 1
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kFpSalt = 0x6C7368626C6F6F6Dull;  // fingerprint salt (DESIGN R1)
+
+// SplitMix64 finaliser (DESIGN R5).
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// h mod P for any 64-bit h (Mersenne fold + one conditional subtract).
+__host__ __device__ __forceinline__ uint64_t mod_p(uint64_t h) {
+  uint64_t x = (h & kP) + (h >> 61);
+  return x >= kP ? x - kP : x;
+}
+
+// (c * s + d) mod P for c, d < P and a 32-bit s (band-hash term).
+__device__ __forceinline__ uint64_t affine32_mod_p(uint64_t c, uint32_t s, uint64_t d) {
+  uint64_t lo = c * (uint64_t)s;
+  uint64_t hi = __umul64hi(c, (uint64_t)s);   // < 2^29
+  uint64_t v = (lo & kP) + ((lo >> 61) | (hi << 3)) + d;   // < 2^61 + 2^32 + 2^61
+  v = (v & kP) + (v >> 61);
+  return v >= kP ? v - kP : v;
+}
+
+// Per-permutation coefficients in the kernel's limb layout: a = a1 * 2^31 + a0 (a0 < 2^31,
+// a1 < 2^30) and b' = b + 1 as two 32-bit words (see minhash eval below).
+struct __align__(16) PermCoef {
+  uint32_t a0, a1, bp0, bp1;
+};
+
+// x = fingerprint mod P split for the eval: xl = x mod 2^30, xh = x >> 30 (< 2^31),
+// xh2 = 2 xh, xl4 = 4 xl (both < 2^32).
+struct __align__(16) XLimbs {
+  uint32_t xl, xh, xh2, xl4;
+};
+
+// Exact 64-bit h mod m with a precomputed inv = floor((2^64-1)/m) (Barrett; corrected).
+__device__ __forceinline__ uint64_t mod_m(uint64_t h, uint64_t m, uint64_t inv) {
+  uint64_t q = __umul64hi(h, inv);
+  uint64_t r = h - q * m;
+  while (r >= m) r -= m;
+  return r;
+}
+
+}  // namespace lb

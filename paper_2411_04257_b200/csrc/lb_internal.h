@@ -1,0 +1,74 @@
+// lb_internal.h -- kernel parameter blocks and launchers shared by the library's .cu files.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "lb_common.cuh"
+
+namespace lb {
+
+constexpr int kMaxBands = 64;
+
+// Where the K1 epilogue writes band hash j of batch document d:
+//   out[blockstart[j] + (d - doc0) * ncol[j] + col[j]]   (skip bands with ncol[j] == 0)
+struct BandMap {
+  uint64_t blockstart[kMaxBands];
+  uint32_t ncol[kMaxBands];
+  uint32_t col[kMaxBands];
+};
+
+struct MinhashParams {
+  const uint64_t* offsets;   // batch offsets (device), n+1
+  const uint32_t* tokens;    // device tokens; document d starts at tokens[offsets[d] - tok_base]
+  uint64_t tok_base;
+  uint32_t doc0;             // first batch document of this launch
+  uint32_t n_docs;           // documents in this launch
+  uint32_t* counter;         // work counter (zeroed before launch)
+  uint32_t shingle_n;
+  uint64_t fp_init_n;        // mix64(kFpSalt + shingle_n)
+  const PermCoef* coef;      // [32 * npl] (padded)
+  uint32_t num_perm;
+  uint32_t* sig_out;         // [n][num_perm] (batch-indexed) or null
+  uint64_t* bh_out;          // band hashes (see BandMap) or null
+  uint32_t b, r;
+  const uint64_t* bcoef;     // c[0..r), d[0..r)
+  BandMap map;
+  const int* err;            // nonzero: batch rejected, do nothing
+};
+
+struct BloomParams {
+  uint32_t* F;               // owned filters, bl * W uint32 words
+  uint32_t* T2;              // contested marks, same layout, all-zero between sub-batches
+  uint64_t W;                // uint32 words per band
+  uint64_t m, m_inv;         // probe modulus and Barrett reciprocal
+  uint32_t k, bl;            // probes, owned bands
+  const uint64_t* s1;        // [bl] filter seeds of the owned bands (global band index)
+  const uint64_t* s2;
+  uint64_t* ekey;            // earliest-setter table (open addressing), cap slots
+  uint64_t* eval;
+  uint32_t ecap_log2;
+  uint64_t gen;              // sub-batch generation tag (1 .. 2^22-1)
+  const uint64_t* bh;        // [n][bl] band hashes of the batch
+  uint32_t i0, nsb;          // sub-batch = batch documents [i0, i0 + nsb)
+  uint64_t* st_g0;           // [nsb * bl] per (doc, band) state
+  uint64_t* st_d;
+  uint64_t* st_pre;
+  uint64_t* st_arr;
+  uint32_t* cand;            // candidate (doc, band) pairs
+  uint32_t* cand_count;
+  uint8_t* dup;              // [n] batch flags (OR over owned bands)
+  const int* err;
+};
+
+struct ErrState {
+  int flags;                 // bit0: usage (offsets[0] != 0 or decreasing)
+  int pad;
+  unsigned long long first_empty;  // first empty document (~0 if none)
+};
+
+// launchers (return number of kernel launches issued)
+int launch_validate(const uint64_t* offsets, uint64_t n_docs, ErrState* err, cudaStream_t s);
+int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s);
+int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s);
+
+}  // namespace lb

@@ -1,0 +1,203 @@
+// lb_minhash.cu -- K1: shingle fingerprints + MinHash + band-hash epilogue (sm_100a).
+//
+// One warp per document (persistent warps pull documents from an atomic counter).  Lanes own
+// permutations p = lane + 32 q (q < NPL): their coefficients stay in registers for the whole
+// launch, the running minima too, so no cross-lane reduction is ever needed.  The warp walks
+// the document's shingles in chunks of 32: lane l fingerprints shingle s0 + l (DESIGN
+// R1) and parks x = fp mod P, pre-split into 30/31-bit limbs, in shared memory; then every
+// lane evaluates its NPL permutations on each of the 32 shingles (a warp-uniform shared-memory
+// broadcast per shingle).
+//
+// The eval (DESIGN R3/R4):  y = ((a x + b) mod P) mod 2^32, exact.
+//   a = a1 2^31 + a0, x = xh 2^30 + xl  =>  a x = a1 xh 2^61 + 2^30 (a0 xh + 2 a1 xl) + a0 xl
+//   2^61 = 1 (mod P)  =>  a x + b + 1 = A + 2^30 G (mod P),
+//       A = a0 xl + a1 xh + (b+1)            (< 3 2^61, two IMAD.WIDE with 64-bit addends)
+//       G' = 2G = a0 (2 xh) + a1 (4 xl)      (< 2^64,   two IMAD.WIDE)
+//   2^30 G = 2^29 G' = G'_hi 2^61 + G'_lo 2^29 = G'_hi + G'_lo 2^29 (mod P)
+//   S' = A + G'_hi + G'_lo 2^29  (< 2^63 + 2^32),  S' = S + 1 with S = a x + b (mod P)
+//   q = floor(S / P) = (S' + (S' >> 61)) >> 61,   y = low32(S - q P) = low32(S') - 1 + q.
+// Four 32x32->64 multiplies (the minimum for a 61x61-bit product; IMAD.WIDE issues at 1/4 rate)
+// plus ~8 ALU ops; tools/micro measured the per-opcode rates.
+#include <cstdint>
+
+#include "lb_internal.h"
+
+namespace lb {
+
+#define K1_THREADS 256
+#define K1_WARPS (K1_THREADS / 32)
+
+__device__ __forceinline__ uint32_t eval_trunc(const PermCoef& c, const XLimbs& x) {
+  uint32_t y;
+  asm("{\n\t"
+      ".reg .u64 A, G, BP;\n\t"
+      ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
+      "mov.b64 BP, {%3, %4};\n\t"
+      "mad.wide.u32 A, %1, %5, BP;\n\t"   // a0*xl + b'
+      "mad.wide.u32 A, %2, %6, A;\n\t"    // + a1*xh
+      "mul.wide.u32 G, %1, %7;\n\t"       // a0*(2xh)
+      "mad.wide.u32 G, %2, %8, G;\n\t"    // + a1*(4xl)
+      "mov.b64 {s0, s1}, A;\n\t"
+      "mov.b64 {g0, g1}, G;\n\t"
+      "shl.b32 t1, g0, 29;\n\t"
+      "shr.u32 t2, g0, 3;\n\t"
+      "add.cc.u32 s0, s0, t1;\n\t"
+      "addc.u32 s1, s1, t2;\n\t"
+      "add.cc.u32 s0, s0, g1;\n\t"
+      "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0
+      "shr.u32 q, s1, 29;\n\t"
+      "add.cc.u32 t1, s0, q;\n\t"
+      "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
+      "shr.u32 q, t2, 29;\n\t"            // q = W >> 61
+      "add.u32 s0, s0, q;\n\t"
+      "sub.u32 %0, s0, 1;\n\t"
+      "}"
+      : "=r"(y)
+      : "r"(c.a0), "r"(c.a1), "r"(c.bp0), "r"(c.bp1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
+  return y;
+}
+
+__device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
+  uint64_t x = mod_p(fp);
+  XLimbs l;
+  l.xl = (uint32_t)x & 0x3FFFFFFFu;
+  l.xh = (uint32_t)(x >> 30);
+  l.xh2 = l.xh << 1;
+  l.xl4 = l.xl << 2;
+  return l;
+}
+
+template <int NPL, int UNR>
+__global__ void __launch_bounds__(K1_THREADS) k1_minhash(const MinhashParams p) {
+  __shared__ XLimbs xs[K1_WARPS][32];
+  __shared__ uint32_t sg[K1_WARPS][32 * NPL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (*p.err) return;
+  PermCoef c[NPL];
+#pragma unroll
+  for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
+
+  for (;;) {
+    uint32_t di = 0;
+    if (lane == 0) di = atomicAdd(p.counter, 1u);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (di >= p.n_docs) break;
+    const uint32_t d = p.doc0 + di;
+    const uint64_t o0 = p.offsets[d];
+    const uint64_t L = p.offsets[d + 1] - o0;
+    const uint32_t* tk = p.tokens + (o0 - p.tok_base);
+    const uint32_t n = p.shingle_n;
+    const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;     // the bag of n-grams
+    const uint32_t t = L >= n ? n : (uint32_t)L;
+    const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
+
+    uint32_t mn[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; q++) mn[q] = 0xFFFFFFFFu;
+
+    for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      if (s < S) {
+        uint64_t h = init;
+        for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)__ldg(tk + s + j));
+        xs[w][lane] = make_limbs(h);
+      }
+      __syncwarp();
+      const uint32_t cnt = min(32u, S - s0);
+      uint32_t j = 0;
+      for (; j + UNR <= cnt; j += UNR) {
+        XLimbs xv[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; u++) xv[u] = xs[w][j + u];
+#pragma unroll
+        for (int q = 0; q < NPL; q++) {
+#pragma unroll
+          for (int u = 0; u < UNR; u += 2) {
+            uint32_t y0 = eval_trunc(c[q], xv[u]);
+            uint32_t y1 = eval_trunc(c[q], xv[u + 1]);
+            mn[q] = min(mn[q], min(y0, y1));
+          }
+        }
+      }
+      for (; j < cnt; j++) {
+        const XLimbs xv = xs[w][j];
+#pragma unroll
+        for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_trunc(c[q], xv));
+      }
+      __syncwarp();
+    }
+
+    if (p.sig_out) {
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const uint32_t pm = lane + 32 * q;
+        if (pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = mn[q];
+      }
+    }
+    if (p.bh_out) {
+#pragma unroll
+      for (int q = 0; q < NPL; q++) sg[w][lane + 32 * q] = mn[q];
+      __syncwarp();
+      for (uint32_t j = lane; j < p.b; j += 32) {
+        if (p.map.ncol[j] == 0) continue;
+        uint64_t acc = 0;                               // BH_j, P:207-208 (DESIGN R6/R7)
+        for (uint32_t u = 0; u < p.r; u++) {
+          acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][j * p.r + u], __ldg(p.bcoef + p.r + u));
+          acc = acc >= kP ? acc - kP : acc;
+        }
+        p.bh_out[p.map.blockstart[j] + (uint64_t)(d - p.doc0) * p.map.ncol[j] + p.map.col[j]] = acc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int NPL, int UNR>
+static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s) {
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR>, K1_THREADS, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
+  uint64_t grid = (uint64_t)sm_count * blocks_per_sm;
+  if (want < grid) grid = want ? want : 1;
+  k1_minhash<NPL, UNR><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  return 1;
+}
+
+int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s) {
+  switch (npl) {
+    case 1: return launch_t<1, 4>(p, sm_count, s);
+    case 2: return launch_t<2, 4>(p, sm_count, s);
+    case 4: return launch_t<4, 4>(p, sm_count, s);
+    case 8: return launch_t<8, 2>(p, sm_count, s);
+    case 16: return launch_t<16, 2>(p, sm_count, s);
+    case 32: return launch_t<32, 2>(p, sm_count, s);
+    default: return -1;
+  }
+}
+
+// K0: CSR validation (S:64 empty document; malformed offsets).
+__global__ void k0_validate(const uint64_t* __restrict__ off, uint64_t n, ErrState* err) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0 && off[0] != 0) atomicOr(&err->flags, 1);
+  if (i < n) {
+    uint64_t a = off[i], b = off[i + 1];
+    if (b < a) atomicOr(&err->flags, 1);
+    else if (b == a) atomicMin(&err->first_empty, (unsigned long long)i);
+  }
+}
+
+__global__ void k0_fold(ErrState* err, int* gate) {
+  *gate = (err->flags != 0 || err->first_empty != ~0ull) ? 1 : 0;
+}
+
+int launch_validate(const uint64_t* offsets, uint64_t n_docs, ErrState* err, cudaStream_t s) {
+  unsigned grid = (unsigned)((n_docs + 255) / 256);
+  k0_validate<<<grid ? grid : 1, 256, 0, s>>>(offsets, n_docs, err);
+  k0_fold<<<1, 1, 0, s>>>(err, &err->pad);
+  return 2;
+}
+
+}  // namespace lb
