@@ -126,6 +126,13 @@ LSHBLOOM_API int lshbloom_signatures(lshbloom *h, const lshbloom_batch *batch, u
 /* Band hashes bh_out[n_docs][b] (uint64, values < 2^61-1) for ALL b bands.  Pure. */
 LSHBLOOM_API int lshbloom_band_hashes(lshbloom *h, const lshbloom_batch *batch, uint64_t *bh_out);
 
+/* Band hashes of ALL b bands laid out for the band-sharded exchange (world > 1): one
+ * contiguous block per owner rank o = 0..world-1, block o = [n_docs][band_hi(o)-band_lo(o)]
+ * (global band j of document d at block_start(o) + d*(hi-lo) + (j-lo)), so that the
+ * all-to-all sends block o to rank o unchanged.  With world = 1 identical to
+ * lshbloom_band_hashes.  Pure. */
+LSHBLOOM_API int lshbloom_band_hashes_sharded(lshbloom *h, const lshbloom_batch *batch, uint64_t *bh_out);
+
 /* Query-then-insert every document of the batch in stream order against the owned band
  * filters (all bands when world = 1): dup_out[d] = 1 iff some owned band's k probe bits
  * were all set before document d (by earlier batches or earlier documents of this batch),
@@ -153,6 +160,13 @@ LSHBLOOM_API int lshbloom_info(const lshbloom *h, lshbloom_info_t *out);
 
 /* Last error message of h (or of the last failed create when h is NULL). */
 LSHBLOOM_API const char *lshbloom_last_error(const lshbloom *h);
+
+/* Stage timing with CUDA events recorded on the call's stream around the MinHash (K1)
+ * launches and the Bloom (K3-K6) sub-batch loop.  enable != 0 turns recording on for later
+ * calls.  ms_out[0] / ms_out[1] receive the K1 / Bloom milliseconds accumulated since the
+ * previous read, n_out[0] / n_out[1] the number of timed K1 launches / Bloom stages; both
+ * accumulators are then reset.  Either pointer may be NULL. */
+LSHBLOOM_API int lshbloom_stage_times(lshbloom *h, int32_t enable, double *ms_out, uint64_t *n_out);
 
 /* Number of kernel launches the library issued since create (launch-count evidence). */
 LSHBLOOM_API uint64_t lshbloom_launch_count(const lshbloom *h);

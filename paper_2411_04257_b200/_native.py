@@ -48,9 +48,9 @@ class _Info(ctypes.Structure):
 
 
 EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloom_signatures",
-           "lshbloom_band_hashes", "lshbloom_query_insert", "lshbloom_query_insert_bands",
-           "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info", "lshbloom_last_error",
-           "lshbloom_launch_count")
+           "lshbloom_band_hashes", "lshbloom_band_hashes_sharded", "lshbloom_query_insert",
+           "lshbloom_query_insert_bands", "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info",
+           "lshbloom_stage_times", "lshbloom_last_error", "lshbloom_launch_count")
 
 
 def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
@@ -63,12 +63,14 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     lib.lshbloom_create_ex.argtypes = [ctypes.POINTER(_Config), ctypes.POINTER(vp)]
     lib.lshbloom_destroy.argtypes = [vp]
     lib.lshbloom_destroy.restype = None
-    for f in ("lshbloom_signatures", "lshbloom_band_hashes", "lshbloom_query_insert"):
+    for f in ("lshbloom_signatures", "lshbloom_band_hashes", "lshbloom_band_hashes_sharded",
+              "lshbloom_query_insert"):
         getattr(lib, f).argtypes = [vp, ctypes.POINTER(_Batch), vp]
     lib.lshbloom_query_insert_bands.argtypes = [vp, vp, u64, i32, vp, vp]
     lib.lshbloom_reset.argtypes = [vp]
     lib.lshbloom_filter_copy.argtypes = [vp, u32, vp]
     lib.lshbloom_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    lib.lshbloom_stage_times.argtypes = [vp, i32, vp, vp]
     lib.lshbloom_last_error.argtypes = [vp]
     lib.lshbloom_last_error.restype = ctypes.c_char_p
     lib.lshbloom_launch_count.argtypes = [vp]
@@ -182,6 +184,20 @@ class LSHBloom:
         out = self._out((n, self.b), np.uint64, _torch_dtype("int64"), dev, offsets)
         self._check(self._lib.lshbloom_band_hashes(self._h, ctypes.byref(bt), self._ptr(out)))
         return out
+
+    def band_hashes_sharded(self, offsets, tokens, *, stream=None):
+        """Band hashes of all bands in owner-major blocks (flat, n*b entries) for the all-to-all."""
+        bt, keep, n, dev = self._batch(offsets, tokens, stream)
+        out = self._out((n * self.b,), np.uint64, _torch_dtype("int64"), dev, offsets)
+        self._check(self._lib.lshbloom_band_hashes_sharded(self._h, ctypes.byref(bt), self._ptr(out)))
+        return out
+
+    def stage_times(self, enable: bool = True):
+        """(K1 ms, Bloom ms), (K1 launches, Bloom stages) since the last read; resets them."""
+        ms = (ctypes.c_double * 2)()
+        nn = (ctypes.c_uint64 * 2)()
+        self._check(self._lib.lshbloom_stage_times(self._h, 1 if enable else 0, ms, nn))
+        return (ms[0], ms[1]), (nn[0], nn[1])
 
     def query_insert(self, offsets, tokens, *, out=None, stream=None):
         """Duplicate flags [n] uint8, stream order; mutates the filters."""

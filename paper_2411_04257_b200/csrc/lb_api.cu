@@ -64,6 +64,12 @@ struct lshbloom {
   ErrState* d_err = nullptr;
   DevBuf off, tok[2], bh, dup, sig;
   uint64_t doc_count = 0, launches = 0;
+  // stage timing (lshbloom_stage_times)
+  bool timing = false;
+  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool pend[2] = {false, false};
+  double stage_ms[2] = {0, 0};
+  uint64_t stage_n[2] = {0, 0};
   std::string err;
   bool poisoned = false;
 };
@@ -120,6 +126,8 @@ void free_all(lshbloom* h) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
   }
+  for (int i = 0; i < 4; i++)
+    if (h->tev[i]) cudaEventDestroy(h->tev[i]);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
 }
@@ -139,6 +147,46 @@ int check_batch(lshbloom* h, const lshbloom_batch* b) {
   if (!b || !b->offsets || !b->tokens) return fail(h, LSHBLOOM_EUSAGE, "NULL batch / offsets / tokens");
   if (b->n_docs == 0 || b->n_docs > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_docs must be in [1, 2^32)");
   return LSHBLOOM_OK;
+}
+
+void stage_begin(lshbloom* h, int st, cudaStream_t s) {
+  if (h->timing) cudaEventRecord(h->tev[2 * st], s);
+}
+void stage_end(lshbloom* h, int st, cudaStream_t s) {
+  if (h->timing) {
+    cudaEventRecord(h->tev[2 * st + 1], s);
+    h->pend[st] = true;
+  }
+}
+// after the stream is synchronised
+void stage_collect(lshbloom* h) {
+  for (int st = 0; st < 2; st++) {
+    if (!h->pend[st]) continue;
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, h->tev[2 * st], h->tev[2 * st + 1]) == cudaSuccess) {
+      h->stage_ms[st] += ms;
+      h->stage_n[st] += 1;
+    }
+    h->pend[st] = false;
+  }
+}
+
+// Owner-major layout for the band-sharded all-to-all (lshbloom_band_hashes_sharded).
+BandMap sharded_map(const lshbloom* h, uint64_t n) {
+  BandMap m;
+  memset(&m, 0, sizeof m);
+  const uint32_t b = h->cfg.b, world = h->cfg.world, base = b / world, rem = b % world;
+  uint64_t start = 0;
+  for (uint32_t o = 0; o < world; o++) {
+    const uint32_t lo = o * base + std::min(o, rem), cnt = base + (o < rem ? 1 : 0);
+    for (uint32_t j = lo; j < lo + cnt; j++) {
+      m.blockstart[j] = start;
+      m.ncol[j] = cnt;
+      m.col[j] = j - lo;
+    }
+    start += n * cnt;
+  }
+  return m;
 }
 
 BandMap owned_map(const lshbloom* h) {
@@ -211,8 +259,10 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
     p.n_docs = (uint32_t)n;
     p.counter = h->d_counters + 1;
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
+    stage_begin(h, 0, s);
     int l = launch_minhash(p, (int)h->npl, h->sm_count, s);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
+    stage_end(h, 0, s);
     h->launches += l;
     LB_CUDA(h, cudaGetLastError());
     return LSHBLOOM_OK;
@@ -231,6 +281,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
   p.offsets = (const uint64_t*)h->off.p;
   uint64_t d0 = 0;
   int c = 0;
+  stage_begin(h, 0, s);
   while (d0 < n) {
     // largest d1 with tokens [off[d0], off[d1]) <= chunk (at least one document)
     const uint64_t t0 = b->offsets[d0];
@@ -258,6 +309,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
     d0 = d1;
     c++;
   }
+  stage_end(h, 0, s);
   return LSHBLOOM_OK;
 }
 
@@ -287,6 +339,7 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t n, uint8_t* dup_dev,
   p.cand_count = h->d_counters;
   p.dup = dup_dev;
   p.err = &h->d_err->pad;
+  stage_begin(h, 1, s);
   for (uint64_t i0 = 0; i0 < n; i0 += SB) {
     if (h->gen >= kGenMax) {   // generation tags exhausted: clear E once every ~4M sub-batches
       const uint64_t cap = 1ull << h->ecap_log2;
@@ -300,12 +353,14 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t n, uint8_t* dup_dev,
     h->launches += launch_bloom_subbatch(p, h->sm_count, s);
     LB_CUDA(h, cudaGetLastError());
   }
+  stage_end(h, 1, s);
   return LSHBLOOM_OK;
 }
 
 int finish(lshbloom* h, cudaStream_t s) {
   LB_CUDA(h, cudaStreamSynchronize(s));
   LB_CUDA(h, cudaGetLastError());
+  stage_collect(h);
   return read_err(h);
 }
 
@@ -392,6 +447,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     CR(cudaEventCreateWithFlags(&h->ev_k1[i], cudaEventDisableTiming));
     CR(cudaEventRecord(h->ev_k1[i], h->own_stream));
   }
+  for (int i = 0; i < 4; i++) CR(cudaEventCreate(&h->tev[i]));
 
   // Hash family (DESIGN R5), in the kernel's limb layout.
   std::vector<PermCoef> coef(32 * npl);
@@ -485,7 +541,7 @@ int lshbloom_signatures(lshbloom* h, const lshbloom_batch* b, uint32_t* sig_out)
   return finish(h, s);
 }
 
-int lshbloom_band_hashes(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_out) {
+static int band_hashes_impl(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_out, bool sharded) {
   int rc = check_handle(h);
   if (rc) return rc;
   if ((rc = check_batch(h, b))) return rc;
@@ -498,9 +554,30 @@ int lshbloom_band_hashes(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_out)
     LB_CUDA(h, ensure(h->bh, bytes));
     dbh = (uint64_t*)h->bh.p;
   }
-  if ((rc = run_minhash(h, b, s, nullptr, dbh, full_map(h)))) return rc;
+  if ((rc = run_minhash(h, b, s, nullptr, dbh, sharded ? sharded_map(h, b->n_docs) : full_map(h)))) return rc;
   if (!b->on_device) LB_CUDA(h, cudaMemcpyAsync(bh_out, dbh, bytes, cudaMemcpyDeviceToHost, s));
   return finish(h, s);
+}
+
+int lshbloom_band_hashes(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_out) {
+  return band_hashes_impl(h, b, bh_out, false);
+}
+
+int lshbloom_band_hashes_sharded(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_out) {
+  return band_hashes_impl(h, b, bh_out, true);
+}
+
+int lshbloom_stage_times(lshbloom* h, int32_t enable, double* ms_out, uint64_t* n_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  h->timing = enable != 0;
+  for (int st = 0; st < 2; st++) {
+    if (ms_out) ms_out[st] = h->stage_ms[st];
+    if (n_out) n_out[st] = h->stage_n[st];
+    h->stage_ms[st] = 0;
+    h->stage_n[st] = 0;
+  }
+  return LSHBLOOM_OK;
 }
 
 int lshbloom_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out) {

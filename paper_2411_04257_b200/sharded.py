@@ -1,0 +1,71 @@
+"""Band-sharded multi-GPU LSHBloom over torch.distributed (north_star).
+
+One process per GPU.  Documents are sharded for MinHash (rank g holds a contiguous range, so
+global stream order = rank order).  Bands are sharded for the Bloom stage: because every
+document inserts all its band hashes (DESIGN R12) each band's filter evolves independently, so
+rank g owns bands [band_lo(g), band_hi(g)) and processes ALL documents of the batch for them.
+Per batch:
+  1. K1 on the local documents writes band hashes owner-major (lshbloom_band_hashes_sharded),
+  2. one all-to-all (NCCL over NVLink) delivers every rank its bands for all documents in
+     global order,
+  3. K3-K6 query-then-insert the owned bands (lshbloom_query_insert_bands),
+  4. one all-reduce(MAX) of the uint8 hit flags combines the bands (any band hits),
+  5. each rank keeps its own documents' flags.
+Results are bit-identical for every world size.  The collectives are plumbing (torch /
+NCCL); every arithmetic step runs in the library's kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def band_range(rank: int, world: int, b: int) -> tuple[int, int]:
+    """Bands owned by `rank`: as even a split as possible, lower ranks take the remainder."""
+    base, rem = divmod(b, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+class ShardedLSHBloom:
+    def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
+                 *, group=None, device: int | None = None, sub_batch: int = 0, engine=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.b = b
+        if engine is None:
+            from ._native import LSHBloom
+            engine = LSHBloom(num_perm, b, r, n_expected, fp_rate, seed, device=device,
+                              rank=self.rank, world=self.world, sub_batch=sub_batch)
+        self.engine = engine
+        self.band_lo, self.band_hi = band_range(self.rank, self.world, b)
+        assert (engine.band_lo, engine.band_hi) == (self.band_lo, self.band_hi)
+        self.bl = self.band_hi - self.band_lo
+        self.widths = [band_range(o, self.world, b)[1] - band_range(o, self.world, b)[0]
+                       for o in range(self.world)]
+
+    def _counts(self, n_local: int, device) -> list[int]:
+        t = torch.tensor([n_local], dtype=torch.int64, device=device)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+    def query_insert(self, offsets, tokens):
+        """Local documents' duplicate flags (uint8), global stream order = rank order."""
+        device = offsets.device
+        n_local = offsets.numel() - 1
+        counts = self._counts(n_local, device)
+        send = self.engine.band_hashes_sharded(offsets, tokens)          # owner-major, flat
+        in_splits = [n_local * w for w in self.widths]
+        out_splits = [c * self.bl for c in counts]
+        recv = torch.empty(sum(out_splits), dtype=send.dtype, device=device)
+        dist.all_to_all_single(recv, send, out_splits, in_splits, group=self.group)
+        n_global = sum(counts)
+        hits = self.engine.query_insert_bands(recv.view(n_global, self.bl))
+        dist.all_reduce(hits, op=dist.ReduceOp.MAX, group=self.group)
+        start = sum(counts[:self.rank])
+        return hits[start:start + n_local]
+
+    def reset(self):
+        self.engine.reset()

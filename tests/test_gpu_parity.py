@@ -242,3 +242,32 @@ def test_query_insert_on_sharded_handle_covers_owned_bands(c1):
                        rank=rank, world=4)
         hits.append(u8(idx.query_insert(*to_dev(off, tok))))
     assert (np.maximum.reduce(hits) == dup).all()
+
+
+def test_band_hashes_sharded_layout(c1):
+    from paper_2411_04257_b200.sharded import band_range
+    cfg, off, tok, sig, bh, dup = c1
+    for world in (1, 3, 8):
+        idx = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=0, rank=0, world=world)
+        got = u64(idx.band_hashes_sharded(*to_dev(off, tok)))
+        want = np.concatenate([np.ascontiguousarray(bh[:, lo:hi]).ravel()
+                               for lo, hi in (band_range(o, world, cfg.b) for o in range(world))])
+        assert (got == want).all()
+
+
+def test_sharded_layer_world1_nccl(c1):
+    import os
+    import torch.distributed as dist
+    from paper_2411_04257_b200.sharded import ShardedLSHBloom
+    cfg, off, tok, sig, bh, dup = c1
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=0)
+        half = 4321
+        a = sx.query_insert(*to_dev(off[:half + 1], tok[:int(off[half])]))
+        b = sx.query_insert(*to_dev(off[half:] - off[half], tok[int(off[half]):]))
+        assert (np.concatenate([u8(a), u8(b)]) == dup).all()
+    finally:
+        dist.destroy_process_group()
