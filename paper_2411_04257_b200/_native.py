@@ -12,7 +12,8 @@ import os
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblshbloom.so")
+_LIB_PATH = os.environ.get("LSHBLOOM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                           "liblshbloom.so")
 
 OK, EUSAGE, EDATA, ERUNTIME, ENOMEM = 0, 1, 2, 3, 4
 

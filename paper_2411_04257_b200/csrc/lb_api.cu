@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -11,6 +12,10 @@
 #include "lb_internal.h"
 
 using namespace lb;
+
+#ifndef LB_MIXMASK
+#define LB_MIXMASK 0x0
+#endif
 
 namespace {
 
@@ -46,7 +51,9 @@ struct lshbloom {
   uint64_t m = 0, m_inv = 0, W = 0;
   uint32_t k = 0, band_lo = 0, band_hi = 0, bl = 0, npl = 0, sub_batch = 0;
   int device = 0, sm_count = 148;
-  cudaStream_t own_stream = nullptr, copy_stream = nullptr;
+  cudaStream_t own_stream = nullptr, copy_stream = nullptr, bloom_stream = nullptr;
+  cudaEvent_t ev_fuse = nullptr;
+  int k1_bps = 0;                 // K1 blocks per SM cap (0 = occupancy limit)
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_k1[2] = {nullptr, nullptr};
   PermCoef* d_coef = nullptr;
   uint64_t* d_bcoef = nullptr;
@@ -128,6 +135,8 @@ void free_all(lshbloom* h) {
   }
   for (int i = 0; i < 4; i++)
     if (h->tev[i]) cudaEventDestroy(h->tev[i]);
+  if (h->ev_fuse) cudaEventDestroy(h->ev_fuse);
+  if (h->bloom_stream) cudaStreamDestroy(h->bloom_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
 }
@@ -230,6 +239,8 @@ MinhashParams base_params(lshbloom* h) {
   MinhashParams p;
   memset(&p, 0, sizeof p);
   p.shingle_n = h->cfg.shingle_n;
+  p.sh29 = 29;
+  p.sh3 = 3;
   p.fp_init_n = mix64(kFpSalt + h->cfg.shingle_n);
   p.coef = h->d_coef;
   p.num_perm = h->cfg.num_perm;
@@ -260,7 +271,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
     p.counter = h->d_counters + 1;
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
     stage_begin(h, 0, s);
-    int l = launch_minhash(p, (int)h->npl, h->sm_count, s);
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     stage_end(h, 0, s);
     h->launches += l;
@@ -301,7 +312,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
     p.n_docs = (uint32_t)(d1 - d0);
     p.counter = h->d_counters + 1 + buf;
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
-    int l = launch_minhash(p, (int)h->npl, h->sm_count, s);
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     h->launches += l;
     LB_CUDA(h, cudaGetLastError());
@@ -314,7 +325,8 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
 }
 
 // K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
-int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t n, uint8_t* dup_dev, cudaStream_t s) {
+int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_end, uint8_t* dup_dev,
+              cudaStream_t s, bool first = true, bool last = true) {
   BloomParams p;
   memset(&p, 0, sizeof p);
   p.F = h->d_F;
@@ -339,8 +351,8 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t n, uint8_t* dup_dev,
   p.cand_count = h->d_counters;
   p.dup = dup_dev;
   p.err = &h->d_err->pad;
-  stage_begin(h, 1, s);
-  for (uint64_t i0 = 0; i0 < n; i0 += SB) {
+  if (first) stage_begin(h, 1, s);
+  for (uint64_t i0 = i_begin; i0 < i_end; i0 += SB) {
     if (h->gen >= kGenMax) {   // generation tags exhausted: clear E once every ~4M sub-batches
       const uint64_t cap = 1ull << h->ecap_log2;
       LB_CUDA(h, cudaMemsetAsync(h->d_ekey, 0, cap * 8, s));
@@ -349,11 +361,90 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t n, uint8_t* dup_dev,
     }
     p.gen = h->gen++;
     p.i0 = (uint32_t)i0;
-    p.nsb = (uint32_t)std::min<uint64_t>(SB, n - i0);
+    p.nsb = (uint32_t)std::min<uint64_t>(SB, i_end - i0);
     h->launches += launch_bloom_subbatch(p, h->sm_count, s);
     LB_CUDA(h, cudaGetLastError());
   }
-  stage_end(h, 1, s);
+  if (last) stage_end(h, 1, s);
+  return LSHBLOOM_OK;
+}
+
+// query_insert: K1 over document chunks on the caller's stream s, each chunk's Bloom
+// sub-batches on bloom_stream as soon as its band hashes exist, so the integer-bound K1 of
+// chunk c+1 overlaps the memory-bound Bloom kernels of chunk c.  Bloom sub-batches stay in
+// document order (one stream), which is all the exact semantics need.
+constexpr uint64_t kFuseDocs = 131072;
+
+int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8_t* ddup) {
+  const uint64_t n = b->n_docs;
+  uint64_t* bh = (uint64_t*)h->bh.p;
+  MinhashParams p = base_params(h);
+  p.bh_out = bh;
+  p.map = owned_map(h);
+  int rc = reset_err(h, s);
+  if (rc) return rc;
+  uint64_t chunk_tokens = 0;
+  if (b->on_device) {
+    h->launches += launch_validate(b->offsets, n, h->d_err, s);
+    p.offsets = b->offsets;
+    p.tokens = b->tokens;
+    p.tok_base = 0;
+  } else {
+    if ((rc = validate_host(h, b->offsets, n))) return rc;
+    LB_CUDA(h, ensure(h->off, (n + 1) * sizeof(uint64_t)));
+    LB_CUDA(h, cudaMemcpyAsync(h->off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    uint64_t maxdoc = 0;
+    for (uint64_t i = 0; i < n; i++) maxdoc = std::max(maxdoc, b->offsets[i + 1] - b->offsets[i]);
+    chunk_tokens = std::max(kChunkTokens, maxdoc);
+    const uint64_t buf_tokens = std::min(chunk_tokens, b->offsets[n]);
+    for (int i = 0; i < 2; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
+    p.offsets = (const uint64_t*)h->off.p;
+  }
+  LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, s));
+  LB_CUDA(h, cudaEventRecord(h->ev_fuse, s));
+  LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
+  p.counter = h->d_counters + 1;
+  uint64_t d0 = 0;
+  int c = 0;
+  stage_begin(h, 0, s);
+  while (d0 < n) {
+    uint64_t d1;
+    if (b->on_device) {
+      d1 = std::min(n, d0 + kFuseDocs);
+    } else {
+      const uint64_t t0 = b->offsets[d0];
+      const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
+      d1 = (uint64_t)(lim - b->offsets) - 1;
+      if (d1 <= d0) d1 = d0 + 1;
+      d1 = std::min(d1, d0 + kFuseDocs);
+      const uint64_t t1 = b->offsets[d1];
+      const int buf = c & 1;
+      LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
+      LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, h->copy_stream));
+      LB_CUDA(h, cudaEventRecord(h->ev_h2d[buf], h->copy_stream));
+      LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_h2d[buf], 0));
+      p.tokens = (const uint32_t*)h->tok[buf].p;
+      p.tok_base = t0;
+    }
+    p.doc0 = (uint32_t)d0;
+    p.n_docs = (uint32_t)(d1 - d0);
+    p.map = owned_map(h);
+    LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
+    if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
+    h->launches += l;
+    LB_CUDA(h, cudaGetLastError());
+    if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[c & 1], s));
+    if (d1 == n) stage_end(h, 0, s);
+    LB_CUDA(h, cudaEventRecord(h->ev_fuse, s));
+    LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
+    if ((rc = run_bloom(h, bh, d0, d1, ddup, h->bloom_stream, d0 == 0, d1 == n))) return rc;
+    d0 = d1;
+    c++;
+  }
+  LB_CUDA(h, cudaEventRecord(h->ev_fuse, h->bloom_stream));
+  LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_fuse, 0));
   return LSHBLOOM_OK;
 }
 
@@ -442,6 +533,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev));
   CR(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
   CR(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  CR(cudaStreamCreateWithFlags(&h->bloom_stream, cudaStreamNonBlocking));
+  CR(cudaEventCreateWithFlags(&h->ev_fuse, cudaEventDisableTiming));
+  if (const char* e = getenv("LSHBLOOM_K1_BPS")) h->k1_bps = atoi(e);
   for (int i = 0; i < 2; i++) {
     CR(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming));
     CR(cudaEventCreateWithFlags(&h->ev_k1[i], cudaEventDisableTiming));
@@ -457,7 +551,14 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
       a = 1 + R(c.seed, 1, 2ull * i) % (kP - 1);
       bb = R(c.seed, 1, 2ull * i + 1) % kP;
     }
-    const uint64_t bp = bb + 1;
+    // slot q = i / 32 of every lane: "b+1" form, or the "cb" form when bit q of LB_MIXMASK is
+    // set: cb = ((b + 1) * 2^32 mod P) + P contributes (b + 1) 2^61 = b + 1 (mod P) once
+    // scaled by 2^29 in the kernel, and being >= P keeps S' >= 1 (lb_minhash.cu).
+    uint64_t bp = bb + 1;
+    if ((LB_MIXMASK >> (i / 32)) & 1) {
+      const uint64_t b1 = (bb + 1 == kP) ? 0 : bb + 1;
+      bp = (uint64_t)(((unsigned __int128)b1 << 32) % kP) + kP;
+    }
     coef[i].a0 = (uint32_t)(a & 0x7FFFFFFFull);
     coef[i].a1 = (uint32_t)(a >> 31);
     coef[i].bp0 = (uint32_t)bp;
@@ -594,9 +695,7 @@ int lshbloom_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out
     LB_CUDA(h, ensure(h->dup, n));
     ddup = (uint8_t*)h->dup.p;
   }
-  if ((rc = run_minhash(h, b, s, nullptr, (uint64_t*)h->bh.p, owned_map(h)))) return rc;
-  LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, s));
-  if ((rc = run_bloom(h, (const uint64_t*)h->bh.p, n, ddup, s))) return rc;
+  if ((rc = run_query_insert(h, b, s, ddup))) return rc;
   if (!b->on_device) LB_CUDA(h, cudaMemcpyAsync(dup_out, ddup, n, cudaMemcpyDeviceToHost, s));
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n;
@@ -623,7 +722,7 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   }
   if ((rc = reset_err(h, s))) return rc;
   LB_CUDA(h, cudaMemsetAsync(dhit, 0, n_docs, s));
-  if ((rc = run_bloom(h, dbh, n_docs, dhit, s))) return rc;
+  if ((rc = run_bloom(h, dbh, 0, n_docs, dhit, s))) return rc;
   if (!on_device) LB_CUDA(h, cudaMemcpyAsync(hit_out, dhit, n_docs, cudaMemcpyDeviceToHost, s));
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n_docs;

@@ -25,6 +25,7 @@ struct MinhashParams {
   uint32_t n_docs;           // documents in this launch
   uint32_t* counter;         // work counter (zeroed before launch)
   uint32_t shingle_n;
+  uint32_t sh29, sh3;         // the constants 29 and 3 (kept opaque to ptxas)
   uint64_t fp_init_n;        // mix64(kFpSalt + shingle_n)
   const PermCoef* coef;      // [32 * npl] (padded)
   uint32_t num_perm;
@@ -68,7 +69,7 @@ struct ErrState {
 
 // launchers (return number of kernel launches issued)
 int launch_validate(const uint64_t* offsets, uint64_t n_docs, ErrState* err, cudaStream_t s);
-int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s);
+int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps);
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s);
 
 }  // namespace lb

@@ -24,36 +24,86 @@
 
 namespace lb {
 
+#ifndef K1_THREADS
 #define K1_THREADS 256
+#endif
+#ifndef LB_K1_MINB
+#define LB_K1_MINB 1
+#endif
+#ifndef LB_UNR4
+#define LB_UNR4 4
+#endif
 #define K1_WARPS (K1_THREADS / 32)
 
-__device__ __forceinline__ uint32_t eval_trunc(const PermCoef& c, const XLimbs& x) {
+// Which permutation slots q (p = lane + 32 q) use the "cb" form (bit q set) rather than the
+// "b+1" form; the host expands the coefficients accordingly (lb_api.cu).  The two forms load
+// the SM's integer pipes differently (fmaheavy vs ALU); mixing them balances the pipes.
+#ifndef LB_MIXMASK
+#define LB_MIXMASK 0x0
+#endif
+
+// Form A ("b+1"):  A = a0 xl + a1 xh + (b+1),  G' = a0 (2xh) + a1 (4xl)
+// Form C ("cb")  :  A = a0 xl + a1 xh,          G' = a0 (2xh) + a1 (4xl) + cb,
+//                   cb = ((b+1) 2^32 mod P) + P  (cb 2^29 = b + 1 mod P; cb >= P keeps S' >= 1)
+// Both: S' = A + G'_hi + G'_lo 2^29 = a x + b + 1 (mod P), 1 <= S' < 2^63.
+__device__ __forceinline__ uint32_t eval_trunc(bool cb, const PermCoef& c, const XLimbs& x,
+                                               uint32_t sh29, uint32_t sh3) {
   uint32_t y;
-  asm("{\n\t"
-      ".reg .u64 A, G, BP;\n\t"
-      ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
-      "mov.b64 BP, {%3, %4};\n\t"
-      "mad.wide.u32 A, %1, %5, BP;\n\t"   // a0*xl + b'
-      "mad.wide.u32 A, %2, %6, A;\n\t"    // + a1*xh
-      "mul.wide.u32 G, %1, %7;\n\t"       // a0*(2xh)
-      "mad.wide.u32 G, %2, %8, G;\n\t"    // + a1*(4xl)
-      "mov.b64 {s0, s1}, A;\n\t"
-      "mov.b64 {g0, g1}, G;\n\t"
-      "shl.b32 t1, g0, 29;\n\t"
-      "shr.u32 t2, g0, 3;\n\t"
-      "add.cc.u32 s0, s0, t1;\n\t"
-      "addc.u32 s1, s1, t2;\n\t"
-      "add.cc.u32 s0, s0, g1;\n\t"
-      "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0
-      "shr.u32 q, s1, 29;\n\t"
-      "add.cc.u32 t1, s0, q;\n\t"
-      "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
-      "shr.u32 q, t2, 29;\n\t"            // q = W >> 61
-      "add.u32 s0, s0, q;\n\t"
-      "sub.u32 %0, s0, 1;\n\t"
-      "}"
-      : "=r"(y)
-      : "r"(c.a0), "r"(c.a1), "r"(c.bp0), "r"(c.bp1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
+  if (!cb) {
+    asm("{\n\t"
+        ".reg .u64 A, G, BP;\n\t"
+        ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
+        "mov.b64 BP, {%3, %4};\n\t"
+        "mad.wide.u32 A, %1, %5, BP;\n\t"
+        "mad.wide.u32 A, %2, %6, A;\n\t"
+        "mul.wide.u32 G, %1, %7;\n\t"
+        "mad.wide.u32 G, %2, %8, G;\n\t"
+        "mov.b64 {s0, s1}, A;\n\t"
+        "mov.b64 {g0, g1}, G;\n\t"
+        "shl.b32 t1, g0, 29;\n\t"
+        "shr.u32 t2, g0, 3;\n\t"
+        "add.cc.u32 s0, s0, t1;\n\t"
+        "addc.u32 s1, s1, t2;\n\t"
+        "add.cc.u32 s0, s0, g1;\n\t"
+        "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0 = S + 1,  S = a x + b (mod P)
+        "shr.u32 q, s1, 29;\n\t"
+        "add.cc.u32 t1, s0, q;\n\t"
+        "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
+        "shr.u32 q, t2, 29;\n\t"            // q = W >> 61 = floor(S / P)
+        "add.u32 s0, s0, q;\n\t"
+        "sub.u32 %0, s0, 1;\n\t"            // low32(S - q P) = low32(S') - 1 + q
+        "}"
+        : "=r"(y)
+        : "r"(c.a0), "r"(c.a1), "r"(c.bp0), "r"(c.bp1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
+  } else {
+    // shift amounts 29 and 3 come from registers so ptxas keeps them on the ALU pipe
+    asm("{\n\t"
+        ".reg .u64 A, G, CB;\n\t"
+        ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
+        "mov.b64 CB, {%3, %4};\n\t"
+        "mul.wide.u32 A, %1, %5;\n\t"
+        "mad.wide.u32 A, %2, %6, A;\n\t"
+        "mad.wide.u32 G, %1, %7, CB;\n\t"
+        "mad.wide.u32 G, %2, %8, G;\n\t"
+        "mov.b64 {s0, s1}, A;\n\t"
+        "mov.b64 {g0, g1}, G;\n\t"
+        "shl.b32 t1, g0, %9;\n\t"
+        "shr.u32 t2, g0, %10;\n\t"
+        "add.cc.u32 s0, s0, t1;\n\t"
+        "addc.u32 s1, s1, t2;\n\t"
+        "add.cc.u32 s0, s0, g1;\n\t"
+        "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0 = S + 1,  S = a x + b (mod P)
+        "shr.u32 q, s1, 29;\n\t"
+        "add.cc.u32 t1, s0, q;\n\t"
+        "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
+        "shr.u32 q, t2, 29;\n\t"            // q = W >> 61 = floor(S / P)
+        "add.u32 s0, s0, q;\n\t"
+        "sub.u32 %0, s0, 1;\n\t"            // low32(S - q P) = low32(S') - 1 + q
+        "}"
+        : "=r"(y)
+        : "r"(c.a0), "r"(c.a1), "r"(c.bp0), "r"(c.bp1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4),
+          "r"(sh29), "r"(sh3));
+  }
   return y;
 }
 
@@ -68,7 +118,7 @@ __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
 }
 
 template <int NPL, int UNR>
-__global__ void __launch_bounds__(K1_THREADS) k1_minhash(const MinhashParams p) {
+__global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
   __shared__ uint32_t sg[K1_WARPS][32 * NPL];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -76,6 +126,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_minhash(const MinhashParams p) 
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
+  const uint32_t sh29 = p.sh29, sh3 = p.sh3;   // 29 and 3, opaque to ptxas
 
   for (;;) {
     uint32_t di = 0;
@@ -113,8 +164,8 @@ __global__ void __launch_bounds__(K1_THREADS) k1_minhash(const MinhashParams p) 
         for (int q = 0; q < NPL; q++) {
 #pragma unroll
           for (int u = 0; u < UNR; u += 2) {
-            uint32_t y0 = eval_trunc(c[q], xv[u]);
-            uint32_t y1 = eval_trunc(c[q], xv[u + 1]);
+            uint32_t y0 = eval_trunc(((LB_MIXMASK >> q) & 1) != 0, c[q], xv[u], sh29, sh3);
+            uint32_t y1 = eval_trunc(((LB_MIXMASK >> q) & 1) != 0, c[q], xv[u + 1], sh29, sh3);
             mn[q] = min(mn[q], min(y0, y1));
           }
         }
@@ -122,7 +173,7 @@ __global__ void __launch_bounds__(K1_THREADS) k1_minhash(const MinhashParams p) 
       for (; j < cnt; j++) {
         const XLimbs xv = xs[w][j];
 #pragma unroll
-        for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_trunc(c[q], xv));
+        for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_trunc(((LB_MIXMASK >> q) & 1) != 0, c[q], xv, sh29, sh3));
       }
       __syncwarp();
     }
@@ -153,27 +204,28 @@ __global__ void __launch_bounds__(K1_THREADS) k1_minhash(const MinhashParams p) 
 }
 
 template <int NPL, int UNR>
-static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s) {
+static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR>, K1_THREADS, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
-  uint64_t grid = (uint64_t)sm_count * blocks_per_sm;
+  const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
+  uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
   k1_minhash<NPL, UNR><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
-int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s) {
+int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps) {
   switch (npl) {
-    case 1: return launch_t<1, 4>(p, sm_count, s);
-    case 2: return launch_t<2, 4>(p, sm_count, s);
-    case 4: return launch_t<4, 4>(p, sm_count, s);
-    case 8: return launch_t<8, 2>(p, sm_count, s);
-    case 16: return launch_t<16, 2>(p, sm_count, s);
-    case 32: return launch_t<32, 2>(p, sm_count, s);
+    case 1: return launch_t<1, 4>(p, sm_count, s, max_bps);
+    case 2: return launch_t<2, 4>(p, sm_count, s, max_bps);
+    case 4: return launch_t<4, LB_UNR4>(p, sm_count, s, max_bps);
+    case 8: return launch_t<8, 2>(p, sm_count, s, max_bps);
+    case 16: return launch_t<16, 2>(p, sm_count, s, max_bps);
+    case 32: return launch_t<32, 2>(p, sm_count, s, max_bps);
     default: return -1;
   }
 }
