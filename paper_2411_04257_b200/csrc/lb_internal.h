@@ -9,8 +9,8 @@ namespace lb {
 
 constexpr int kMaxBands = 64;
 
-// Where the K1 epilogue writes band hash j of batch document d:
-//   out[blockstart[j] + (d - doc0) * ncol[j] + col[j]]   (skip bands with ncol[j] == 0)
+// Where the K1 epilogue writes band hash j of batch document d (d indexes the whole batch,
+// not the launch's chunk):  out[blockstart[j] + d * ncol[j] + col[j]]  (skip ncol[j] == 0)
 struct BandMap {
   uint64_t blockstart[kMaxBands];
   uint32_t ncol[kMaxBands];

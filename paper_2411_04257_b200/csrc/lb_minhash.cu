@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
           acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][j * p.r + u], __ldg(p.bcoef + p.r + u));
           acc = acc >= kP ? acc - kP : acc;
         }
-        p.bh_out[p.map.blockstart[j] + (uint64_t)(d - p.doc0) * p.map.ncol[j] + p.map.col[j]] = acc;
+        p.bh_out[p.map.blockstart[j] + (uint64_t)d * p.map.ncol[j] + p.map.col[j]] = acc;
       }
       __syncwarp();
     }

@@ -271,3 +271,17 @@ def test_sharded_layer_world1_nccl(c1):
         assert (np.concatenate([u8(a), u8(b)]) == dup).all()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("on_device", [True, False])
+def test_many_chunks_short_docs(on_device):
+    # > 2 fused K1/Bloom chunks (131072 docs each) and, on the host path, > 1 staging chunk
+    from synthetic.corpus import CorpusConfig, LengthDist
+    cfg = CorpusConfig("short", 300_000, LengthDist(60, 30), 5000, 1.1, 0.1, "edit", 0.0, 0.1,
+                       num_perm=64, b=8, r=8, fp_rate=1e-4)
+    off, tok = gen_range(cfg, 0, cfg.n_docs)
+    _, bh, dup, _ = oracle.run(off, tok, num_perm=64, b=8, r=8, n_expected=cfg.n_docs, fp_rate=1e-4, seed=3)
+    idx = LSHBloom(64, 8, 8, cfg.n_docs, 1e-4, 3, device=0, sub_batch=50_000)
+    args = to_dev(off, tok) if on_device else (off, tok)
+    assert (u8(idx.query_insert(*args)) == dup).all()
+    assert (u64(idx.band_hashes(*args)) == bh).all()
