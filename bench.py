@@ -346,7 +346,7 @@ def main():
                    "n_expected": n_total, "docs_per_step": n_total, "tokens_per_rank": int(len(tok)),
                    "parallelism": "band-sharded x%d" % world if world > 1 else "single GPU",
                    "l2": "inputs %.0f MB > 126 MB L2; filters zeroed each step" % (tok.nbytes / 1e6),
-                   "sub_batch": args.sub_batch or 65536, "csr_checksum_rank0": csum,
+                   "sub_batch": args.sub_batch or 32768, "csr_checksum_rank0": csum,
                    "dup_frac": dup_frac, "gen_s": round(gen_s, 1)},
         "roofline": roofline,
         "stages_ms_per_step": {"minhash_k1": k1_ms / max(1, args.steps), "bloom_k3_k6": bl_ms / max(1, args.steps)},

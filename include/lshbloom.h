@@ -90,7 +90,7 @@ typedef struct {
     int32_t device;      /* CUDA device ordinal, -1 = current */
     uint32_t rank;       /* band sharding: this rank owns bands [band_lo, band_hi) */
     uint32_t world;      /*   over world ranks (bands split as evenly as possible) */
-    uint32_t sub_batch;  /* documents per Bloom sub-batch (0 = default 65536); results do
+    uint32_t sub_batch;  /* documents per Bloom sub-batch (0 = default 32768); results do
                             not depend on it */
 } lshbloom_config;
 

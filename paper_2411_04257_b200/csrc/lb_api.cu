@@ -37,7 +37,7 @@ cudaError_t ensure(DevBuf& b, size_t bytes) {
 
 thread_local std::string g_create_error;
 
-constexpr uint32_t kDefaultSubBatch = 65536;
+constexpr uint32_t kDefaultSubBatch = 32768;
 constexpr uint64_t kChunkTokens = 16ull << 20;   // host-batch staging chunk (64 MB of tokens)
 constexpr uint64_t kGenMax = (1ull << 22) - 1;
 
@@ -60,12 +60,13 @@ struct lshbloom {
   uint64_t* d_s1 = nullptr;
   uint64_t* d_s2 = nullptr;
   uint32_t* d_F = nullptr;
-  uint32_t* d_T2 = nullptr;
+  uint64_t* d_Q = nullptr;        // 2 compact earliest-setter tables of 2^q_log2 slots
+  uint32_t q_log2 = 20;
   uint64_t* d_ekey = nullptr;
   uint64_t* d_eval = nullptr;
   uint32_t ecap_log2 = 0;
   uint64_t gen = 1;
-  uint64_t* d_st = nullptr;       // 4 * sub_batch * bl
+  uint64_t* d_st = nullptr;       // 2 * sub_batch * bl
   uint32_t* d_cand = nullptr;     // sub_batch * bl
   uint32_t* d_counters = nullptr; // [0] candidates, [1..2] K1 work counters
   ErrState* d_err = nullptr;
@@ -126,7 +127,7 @@ int check_handle(lshbloom* h) {
 
 void free_all(lshbloom* h) {
   auto F = [](void* p) { if (p) cudaFree(p); };
-  F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_T2); F(h->d_ekey);
+  F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_ekey);
   F(h->d_eval); F(h->d_st); F(h->d_cand); F(h->d_counters); F(h->d_err);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p);
   for (int i = 0; i < 2; i++) {
@@ -330,7 +331,7 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_
   BloomParams p;
   memset(&p, 0, sizeof p);
   p.F = h->d_F;
-  p.T2 = h->d_T2;
+  p.q_log2 = h->q_log2;
   p.W = h->W;
   p.m = h->m;
   p.m_inv = h->m_inv;
@@ -343,10 +344,8 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_
   p.ecap_log2 = h->ecap_log2;
   p.bh = bh_dev;
   const uint64_t SB = h->sub_batch;
-  p.st_g0 = h->d_st;
-  p.st_d = h->d_st + SB * h->bl;
-  p.st_pre = h->d_st + 2 * SB * h->bl;
-  p.st_arr = h->d_st + 3 * SB * h->bl;
+  p.st_pre = h->d_st;
+  p.st_arr = h->d_st + SB * h->bl;
   p.cand = h->d_cand;
   p.cand_count = h->d_counters;
   p.dup = dup_dev;
@@ -360,6 +359,9 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_
       h->gen = 1;
     }
     p.gen = h->gen++;
+    const uint64_t qslots = 1ull << h->q_log2;
+    p.Q = h->d_Q + (p.gen & 1) * qslots;
+    p.Q_prev = h->d_Q + ((p.gen + 1) & 1) * qslots;
     p.i0 = (uint32_t)i0;
     p.nsb = (uint32_t)std::min<uint64_t>(SB, i_end - i0);
     h->launches += launch_bloom_subbatch(p, h->sm_count, s);
@@ -374,6 +376,15 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_
 // chunk c+1 overlaps the memory-bound Bloom kernels of chunk c.  Bloom sub-batches stay in
 // document order (one stream), which is all the exact semantics need.
 constexpr uint64_t kFuseDocs = 131072;
+constexpr uint64_t kFuseEdgeDocs = 32768;   // small first / last chunks: Bloom starts early, short tail
+
+uint64_t fuse_chunk_end(uint64_t d0, uint64_t n) {
+  if (d0 == 0) return std::min(n, kFuseEdgeDocs);
+  const uint64_t left = n - d0;
+  if (left <= kFuseEdgeDocs) return n;
+  if (left <= kFuseDocs + kFuseEdgeDocs) return n - kFuseEdgeDocs;
+  return d0 + kFuseDocs;
+}
 
 int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8_t* ddup) {
   const uint64_t n = b->n_docs;
@@ -410,13 +421,13 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   while (d0 < n) {
     uint64_t d1;
     if (b->on_device) {
-      d1 = std::min(n, d0 + kFuseDocs);
+      d1 = fuse_chunk_end(d0, n);
     } else {
       const uint64_t t0 = b->offsets[d0];
       const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
       d1 = (uint64_t)(lim - b->offsets) - 1;
       if (d1 <= d0) d1 = d0 + 1;
-      d1 = std::min(d1, d0 + kFuseDocs);
+      d1 = std::min(d1, fuse_chunk_end(d0, n));
       const uint64_t t1 = b->offsets[d1];
       const int buf = c & 1;
       LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
@@ -494,7 +505,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
 
   // Sizing, P:224-225 / S:263 (DESIGN R9): natural log, ceil for m, llround for k.
   const double md = ceil(-(double)c.n_expected * log(c.fp_rate) / (log(2.0) * log(2.0)));
-  if (!(md >= 1.0) || md > 68719476736.0) return fail(nullptr, LSHBLOOM_EUSAGE, "filter size m must be <= 2^36 bits");
+  if (!(md >= 1.0) || md >= 68719476736.0) return fail(nullptr, LSHBLOOM_EUSAGE, "filter size m must be < 2^36 bits");
   long long kk = llround((md / (double)c.n_expected) * log(2.0));
   if (kk < 1) kk = 1;
   if (kk > LSHBLOOM_MAX_K) return fail(nullptr, LSHBLOOM_EUSAGE, "k > 64 probes (fp_rate too small)");
@@ -512,7 +523,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   uint32_t npl = 1;
   while (npl * 32 < c.num_perm) npl *= 2;
   h->npl = npl;
-  h->sub_batch = c.sub_batch ? c.sub_batch : kDefaultSubBatch;
+  h->sub_batch = c.sub_batch ? std::min<uint32_t>(c.sub_batch, 1u << 22) : kDefaultSubBatch;   // doc offsets: 22 bits in Q
 
   int dev = c.device;
   if (dev < 0) cudaGetDevice(&dev);
@@ -535,6 +546,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
   CR(cudaStreamCreateWithFlags(&h->bloom_stream, cudaStreamNonBlocking));
   CR(cudaEventCreateWithFlags(&h->ev_fuse, cudaEventDisableTiming));
+  h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
   if (const char* e = getenv("LSHBLOOM_K1_BPS")) h->k1_bps = atoi(e);
   for (int i = 0; i < 2; i++) {
     CR(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming));
@@ -583,12 +595,12 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaMemcpy(h->d_s1, s1.data(), h->bl * 8, cudaMemcpyHostToDevice));
   CR(cudaMemcpy(h->d_s2, s2.data(), h->bl * 8, cudaMemcpyHostToDevice));
 
-  // Filters "with all bits initially set to 0" and the contested-mark bitmap.
+  // Filters "with all bits initially set to 0".
   const size_t fbytes = (size_t)h->bl * h->W * 4;
   CR(cudaMalloc(&h->d_F, fbytes));
   CR(cudaMemset(h->d_F, 0, fbytes));
-  CR(cudaMalloc(&h->d_T2, fbytes));
-  CR(cudaMemset(h->d_T2, 0, fbytes));
+  CR(cudaMalloc(&h->d_Q, 2 * (8ull << h->q_log2)));
+  CR(cudaMemset(h->d_Q, 0xFF, 2 * (8ull << h->q_log2)));   // all slots empty (~0)
 
   // Earliest-setter table: >= 2x the most contested positions a sub-batch can produce
   // (each contested position has >= 2 of the sub_batch * bl * k probes).
@@ -600,7 +612,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaMalloc(&h->d_eval, (8ull << lg)));
   CR(cudaMemset(h->d_ekey, 0, (8ull << lg)));
   CR(cudaMemset(h->d_eval, 0, (8ull << lg)));
-  CR(cudaMalloc(&h->d_st, 4ull * h->sub_batch * h->bl * 8));
+  CR(cudaMalloc(&h->d_st, 2ull * h->sub_batch * h->bl * 8));
   CR(cudaMalloc(&h->d_cand, (size_t)h->sub_batch * h->bl * 4));
   CR(cudaMalloc(&h->d_counters, 16 * 4));
   CR(cudaMemset(h->d_counters, 0, 16 * 4));

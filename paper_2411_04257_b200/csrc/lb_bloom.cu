@@ -9,28 +9,37 @@
 //   K3 probe   : positions g_t = (h1 + t h2) mod m, read F_pre; all k set -> hit.
 //   K4 insert  : atomicOr every pre-unset probe.  The one atomic that sees the bit clear is the
 //                position's first arrival; every other arrival sees it set -> the position is
-//                contested: mark it in T2 and atomicMax its earliest-setter entry in E.
-//   K5 resolve : each first arrival looks its position up in T2 (then clears it): if contested
-//                it adds itself to E; if not, it is the position's sole prober, so its band
-//                misses (E[p] = i).  Bands whose every pre-unset probe is contested become
-//                candidates.
-//   K6 verdict : candidate hit <=> E[p] < i for every pre-unset probe p.
-// E is an open-addressed table keyed by (generation, band, position) holding
-// (generation << 32 | ~i) under atomicMax (newest generation wins, then the smallest i), so it
-// never needs clearing; T2 is cleared bit by bit by the first arrivals in K5.
+//                contested: the arrival enters itself in E (earliest setter, atomicMin).
+//   K5 resolve : each first arrival looks its position up in E: if present (contested) it joins
+//                the minimum; if absent it is the position's sole prober, so its band misses
+//                (E[p] = i).  Bands whose every pre-unset probe is contested become candidates.
+//   K6 verdict : candidate hit <=> E[p] < i for every pre-unset probe p; then clear the
+//                previous sub-batch's E buffer.
+// E holds only contested positions.  Its primary form Q is a compact open-addressed table of
+// packed u64 slots ((band, position) << 22 | doc - i0; atomicMin keeps the earliest doc), two
+// buffers alternating by sub-batch, small enough to stay L2-resident.  A key whose probe
+// sequence in Q is full (64 slots) lives in the overflow table instead -- consistently, since
+// slots are never freed within a sub-batch -- a worst-case-sized table keyed by
+// (generation, band, position) holding (generation << 32 | ~doc) under atomicMax, which never
+// needs clearing.  Probe positions are recomputed from the band hash in every kernel.
 #include <cstdint>
 
 #include "lb_internal.h"
 
 namespace lb {
 
-#define BL_THREADS 256
+#ifndef BL_THREADS
+#define BL_THREADS 128
+#endif
 
-__device__ __forceinline__ uint64_t ekey_of(uint64_t gen, uint32_t jl, uint64_t g) {
-  return (gen << 42) | ((uint64_t)jl << 36) | g;
-}
 __device__ __forceinline__ uint64_t eslot(uint64_t key, uint32_t log2cap) {
   return (key * 0x9E3779B97F4A7C15ull) >> (64 - log2cap);
+}
+constexpr uint64_t kQEmpty = ~0ull;
+constexpr int kQProbe = 64;
+__device__ __forceinline__ uint64_t qkey(uint32_t jl, uint64_t g) { return ((uint64_t)jl << 36) | g; }
+__device__ __forceinline__ uint64_t qslot(const BloomParams& p, uint64_t key) {
+  return (key * 0xD6E8FEB86659FD93ull) >> (64 - p.q_log2);
 }
 
 // Insert-or-update: E[key] = max(E[key], tag).  Stale (older-generation) slots count as empty.
@@ -70,92 +79,173 @@ __device__ uint32_t e_lookup(const BloomParams& p, uint64_t key) {
   }
 }
 
+// K4: enter doc i as a setter of contested key (earliest wins).
+__device__ void e_add(const BloomParams& p, uint64_t key, uint32_t i) {
+  const uint64_t packed = (key << 22) | (uint64_t)(i - p.i0);
+  const uint64_t mask = (1ull << p.q_log2) - 1;
+  uint64_t s = qslot(p, key);
+  for (int n = 0; n < kQProbe; n++, s = (s + 1) & mask) {
+    uint64_t cur = __ldcg(p.Q + s);
+    if (cur == kQEmpty) {
+      cur = atomicCAS((unsigned long long*)(p.Q + s), (unsigned long long)kQEmpty, (unsigned long long)packed);
+      if (cur == kQEmpty) return;                       // claimed the slot
+    }
+    if ((cur >> 22) == key) {
+      atomicMin((unsigned long long*)(p.Q + s), (unsigned long long)packed);
+      return;
+    }
+  }
+  e_upsert(p, (p.gen << 42) | key, (p.gen << 32) | (uint64_t)(~i));   // overflow table
+}
+
+// K5: if key is contested (present in E), join its minimum with doc i and return true.
+__device__ bool e_join(const BloomParams& p, uint64_t key, uint32_t i) {
+  const uint64_t packed = (key << 22) | (uint64_t)(i - p.i0);
+  const uint64_t mask = (1ull << p.q_log2) - 1;
+  uint64_t s = qslot(p, key);
+  for (int n = 0; n < kQProbe; n++, s = (s + 1) & mask) {
+    const uint64_t cur = __ldcg(p.Q + s);
+    if (cur == kQEmpty) return false;
+    if ((cur >> 22) == key) {
+      atomicMin((unsigned long long*)(p.Q + s), (unsigned long long)packed);
+      return true;
+    }
+  }
+  if (e_lookup(p, (p.gen << 42) | key) == 0xFFFFFFFFu) return false;
+  e_upsert(p, (p.gen << 42) | key, (p.gen << 32) | (uint64_t)(~i));
+  return true;
+}
+
+// K6: earliest setter of key (batch document index), ~0u if absent.
+__device__ uint32_t e_find(const BloomParams& p, uint64_t key) {
+  const uint64_t mask = (1ull << p.q_log2) - 1;
+  uint64_t s = qslot(p, key);
+  for (int n = 0; n < kQProbe; n++, s = (s + 1) & mask) {
+    const uint64_t cur = __ldcg(p.Q + s);
+    if (cur == kQEmpty) return 0xFFFFFFFFu;
+    if ((cur >> 22) == key) return p.i0 + (uint32_t)(cur & 0x3FFFFFull);
+  }
+  return e_lookup(p, (p.gen << 42) | key);
+}
+
+// Probe positions of one band hash: g_t = (h1 + t h2) mod m computed as g_0 = h1 mod m,
+// g_{t+1} = g_t + (h2 mod m) - m [if >= m]  (exact; no 2^64 wrap, DESIGN R10).
+// KT > 0: k = KT known at compile time, positions in registers; KT = 0: runtime k <= 64.
+struct ProbeGen {   // sequential positions (any k)
+  uint64_t x, dl, m;
+  __device__ __forceinline__ ProbeGen(const BloomParams& p, uint64_t bh, uint32_t jl) {
+    const uint64_t h1 = mix64(bh ^ p.s1[jl]);
+    const uint64_t h2 = mix64(bh ^ p.s2[jl]) | 1ull;
+    x = mod_m(h1, p.m, p.m_inv);
+    dl = mod_m(h2, p.m, p.m_inv);
+    m = p.m;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t g = x;
+    x += dl;
+    x = x >= m ? x - m : x;
+    return g;
+  }
+};
+
+template <int KT>   // KT > 0: all k positions in registers
+struct Probes {
+  uint64_t g[KT];
+  __device__ __forceinline__ Probes(const BloomParams& p, uint64_t bh, uint32_t jl) {
+    ProbeGen gen(p, bh, jl);
+#pragma unroll
+    for (int t = 0; t < KT; t++) g[t] = gen.next();
+  }
+};
+
+__device__ __forceinline__ uint64_t full_mask(uint32_t k) { return k == 64 ? ~0ull : ((1ull << k) - 1); }
+
 // K3: probe positions + pre-sub-batch test.
+template <int KT>
 __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
   const uint32_t jl = (uint32_t)(idx % p.bl);
   const uint32_t i = p.i0 + (uint32_t)(idx / p.bl);
   const uint64_t bh = p.bh[(uint64_t)i * p.bl + jl];
-  const uint64_t h1 = mix64(bh ^ p.s1[jl]);
-  const uint64_t h2 = mix64(bh ^ p.s2[jl]) | 1ull;
-  const uint64_t g0 = mod_m(h1, p.m, p.m_inv);
-  const uint64_t dl = mod_m(h2, p.m, p.m_inv);
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
-  uint64_t pre = 0, g = g0;
-#pragma unroll 4
-  for (uint32_t t = 0; t < p.k; t++) {
-    const uint32_t w = __ldcg(F + (g >> 5));
-    pre |= (uint64_t)((w >> (g & 31)) & 1u) << t;
-    g += dl;
-    g = g >= p.m ? g - p.m : g;
+  uint64_t pre = 0;
+  if constexpr (KT > 0) {
+    const Probes<KT> pr(p, bh, jl);
+    uint32_t w[KT];
+#pragma unroll
+    for (int t = 0; t < KT; t++) w[t] = __ldcg(F + (pr.g[t] >> 5));   // all loads in flight
+#pragma unroll
+    for (int t = 0; t < KT; t++) pre |= (uint64_t)((w[t] >> (pr.g[t] & 31)) & 1u) << t;
+  } else {
+    ProbeGen gen(p, bh, jl);
+    for (uint32_t t = 0; t < p.k; t++) {
+      const uint64_t g = gen.next();
+      pre |= (uint64_t)((__ldcg(F + (g >> 5)) >> (g & 31)) & 1u) << t;
+    }
   }
-  p.st_g0[idx] = g0;
-  p.st_d[idx] = dl;
   p.st_pre[idx] = pre;
-  const uint64_t full = (p.k == 64) ? ~0ull : ((1ull << p.k) - 1);
-  if (pre == full) p.dup[i] = 1;
+  if (pre == full_mask(p.k)) p.dup[i] = 1;
 }
 
 // K4: insert pre-unset probes; detect contested positions.
+template <int KT>
 __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
-  const uint64_t full = (p.k == 64) ? ~0ull : ((1ull << p.k) - 1);
   const uint64_t pre = p.st_pre[idx];
-  if (pre == full) return;
+  if (pre == full_mask(p.k)) return;
   const uint32_t jl = (uint32_t)(idx % p.bl);
   const uint32_t i = p.i0 + (uint32_t)(idx / p.bl);
+  const uint64_t bh = p.bh[(uint64_t)i * p.bl + jl];
   uint32_t* F = p.F + (uint64_t)jl * p.W;
-  uint32_t* T2 = p.T2 + (uint64_t)jl * p.W;
-  const uint64_t dl = p.st_d[idx];
-  const uint64_t tag = (p.gen << 32) | (uint64_t)(~i);
-  uint64_t g = p.st_g0[idx], arr = 0;
-  for (uint32_t t = 0; t < p.k; t++) {
-    if (!((pre >> t) & 1)) {
-      const uint32_t bit = 1u << (g & 31);
-      const uint32_t old = atomicOr(F + (g >> 5), bit);
-      if (old & bit) {
-        atomicOr(T2 + (g >> 5), bit);
-        e_upsert(p, ekey_of(p.gen, jl, g), tag);
-      } else {
-        arr |= 1ull << t;
-      }
+  uint64_t arr = 0;
+  auto settle = [&](uint32_t t, uint64_t g, uint32_t old) {
+    const uint32_t bit = 1u << (g & 31);
+    if (old & bit) {                     // someone else set it in this sub-batch: contested
+      e_add(p, qkey(jl, g), i);
+    } else {
+      arr |= 1ull << t;                  // first arrival
     }
-    g += dl;
-    g = g >= p.m ? g - p.m : g;
+  };
+  if constexpr (KT > 0) {
+    const Probes<KT> pr(p, bh, jl);
+    uint32_t old[KT];
+#pragma unroll
+    for (int t = 0; t < KT; t++)         // all atomics in flight before any result is used
+      old[t] = ((pre >> t) & 1) ? 0u : atomicOr(F + (pr.g[t] >> 5), 1u << (pr.g[t] & 31));
+#pragma unroll
+    for (int t = 0; t < KT; t++)
+      if (!((pre >> t) & 1)) settle(t, pr.g[t], old[t]);
+  } else {
+    ProbeGen gen(p, bh, jl);
+    for (uint32_t t = 0; t < p.k; t++) {
+      const uint64_t g = gen.next();
+      if (!((pre >> t) & 1)) settle(t, g, atomicOr(F + (g >> 5), 1u << (g & 31)));
+    }
   }
   p.st_arr[idx] = arr;
 }
 
-// K5: first arrivals consult T2; contested ones join E; sole probers make the band miss.
+// K5: first arrivals consult C; contested ones join E; sole probers make the band miss.
+template <int KT>
 __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
-  const uint64_t full = (p.k == 64) ? ~0ull : ((1ull << p.k) - 1);
   const uint64_t pre = p.st_pre[idx];
-  if (pre == full) return;
+  if (pre == full_mask(p.k)) return;
   const uint64_t arr = p.st_arr[idx];
   const uint32_t jl = (uint32_t)(idx % p.bl);
   const uint32_t i = p.i0 + (uint32_t)(idx / p.bl);
-  uint32_t* T2 = p.T2 + (uint64_t)jl * p.W;
   bool maybe = true;
   if (arr) {
-    const uint64_t dl = p.st_d[idx];
-    const uint64_t tag = (p.gen << 32) | (uint64_t)(~i);
-    uint64_t g = p.st_g0[idx];
+    const uint64_t bh = p.bh[(uint64_t)i * p.bl + jl];
+    // (not early-exiting: every contested first arrival must join E for the other docs)
+    ProbeGen gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
-      if ((arr >> t) & 1) {
-        const uint32_t bit = 1u << (g & 31);
-        if (__ldcg(T2 + (g >> 5)) & bit) {
-          e_upsert(p, ekey_of(p.gen, jl, g), tag);
-          atomicAnd(T2 + (g >> 5), ~bit);
-        } else {
-          maybe = false;   // only this document probes g: not set before it
-        }
-      }
-      g += dl;
-      g = g >= p.m ? g - p.m : g;
+      const uint64_t g = gen.next();
+      if ((arr >> t) & 1)
+        if (!e_join(p, qkey(jl, g), i)) maybe = false;   // sole prober: not set before i
     }
   }
   if (maybe) {
@@ -164,35 +254,43 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   }
 }
 
-// K6: verdict for candidate (doc, band) pairs.
+// K6: verdict for candidate (doc, band) pairs; then zero the previous sub-batch's C buffer.
+template <int KT>
 __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
   if (*p.err) return;
   const uint32_t nc = *p.cand_count;
-  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += stride) {
     const uint32_t idx = p.cand[c];
     const uint32_t jl = idx % p.bl;
     const uint32_t i = p.i0 + idx / p.bl;
     const uint64_t pre = p.st_pre[idx];
-    const uint64_t dl = p.st_d[idx];
-    uint64_t g = p.st_g0[idx];
+    ProbeGen gen(p, p.bh[(uint64_t)i * p.bl + jl], jl);
     bool hit = true;
     for (uint32_t t = 0; t < p.k && hit; t++) {
-      if (!((pre >> t) & 1)) hit = e_lookup(p, ekey_of(p.gen, jl, g)) < i;
-      g += dl;
-      g = g >= p.m ? g - p.m : g;
+      const uint64_t g = gen.next();
+      if (!((pre >> t) & 1)) hit = e_find(p, qkey(jl, g)) < i;
     }
     if (hit) p.dup[i] = 1;
   }
+  const uint64_t slots = 1ull << p.q_log2;
+  for (uint64_t w = blockIdx.x * blockDim.x + threadIdx.x; w < slots; w += stride) p.Q_prev[w] = kQEmpty;
+}
+
+template <int KT>
+static void launch_k(const BloomParams& p, unsigned grid, int sm_count, cudaStream_t s) {
+  k3_probe<KT><<<grid, BL_THREADS, 0, s>>>(p);
+  k4_insert<KT><<<grid, BL_THREADS, 0, s>>>(p);
+  k5_resolve<KT><<<grid, BL_THREADS, 0, s>>>(p);
+  k6_verdict<KT><<<(unsigned)sm_count * 2, BL_THREADS, 0, s>>>(p);
 }
 
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
   const uint64_t n = (uint64_t)p.nsb * p.bl;
   const unsigned grid = (unsigned)((n + BL_THREADS - 1) / BL_THREADS);
   cudaMemsetAsync(p.cand_count, 0, sizeof(uint32_t), s);
-  k3_probe<<<grid, BL_THREADS, 0, s>>>(p);
-  k4_insert<<<grid, BL_THREADS, 0, s>>>(p);
-  k5_resolve<<<grid, BL_THREADS, 0, s>>>(p);
-  k6_verdict<<<(unsigned)sm_count, BL_THREADS, 0, s>>>(p);
+  if (p.k == 17) launch_k<17>(p, grid, sm_count, s);   // every BASELINE config (p = 1e-5)
+  else launch_k<0>(p, grid, sm_count, s);
   return 4;
 }
 

@@ -39,22 +39,22 @@ struct MinhashParams {
 
 struct BloomParams {
   uint32_t* F;               // owned filters, bl * W uint32 words
-  uint32_t* T2;              // contested marks, same layout, all-zero between sub-batches
+  uint64_t* Q;               // compact earliest-setter table of this sub-batch (2^q_log2 slots)
+  uint64_t* Q_prev;          // the other buffer (previous sub-batch), reset to empty by K6
+  uint32_t q_log2;
   uint64_t W;                // uint32 words per band
   uint64_t m, m_inv;         // probe modulus and Barrett reciprocal
   uint32_t k, bl;            // probes, owned bands
   const uint64_t* s1;        // [bl] filter seeds of the owned bands (global band index)
   const uint64_t* s2;
-  uint64_t* ekey;            // earliest-setter table (open addressing), cap slots
+  uint64_t* ekey;            // overflow earliest-setter table (open addressing), 2^ecap_log2 slots
   uint64_t* eval;
   uint32_t ecap_log2;
   uint64_t gen;              // sub-batch generation tag (1 .. 2^22-1)
   const uint64_t* bh;        // [n][bl] band hashes of the batch
   uint32_t i0, nsb;          // sub-batch = batch documents [i0, i0 + nsb)
-  uint64_t* st_g0;           // [nsb * bl] per (doc, band) state
-  uint64_t* st_d;
-  uint64_t* st_pre;
-  uint64_t* st_arr;
+  uint64_t* st_pre;          // [nsb * bl] per (doc, band): pre-set probe mask (K3)
+  uint64_t* st_arr;          //   and first-arrival probe mask (K4)
   uint32_t* cand;            // candidate (doc, band) pairs
   uint32_t* cand_count;
   uint8_t* dup;              // [n] batch flags (OR over owned bands)
