@@ -54,6 +54,10 @@ extern "C" {
 #define LSHBLOOM_EDATA 2
 #define LSHBLOOM_ERUNTIME 3
 #define LSHBLOOM_ENOMEM 4
+#define LSHBLOOM_EFORMAT 5     /* checkpoint: bad magic / unsupported version / inconsistent header */
+#define LSHBLOOM_ETRUNC 6      /* checkpoint: file shorter than its header says */
+#define LSHBLOOM_ECHECKSUM 7   /* checkpoint: CRC32C mismatch */
+#define LSHBLOOM_EIO 8         /* checkpoint: open / read / write failure */
 
 #define LSHBLOOM_MAX_BANDS 64   /* bands per handle */
 #define LSHBLOOM_MAX_PERM 1024  /* num_perm */
@@ -167,6 +171,23 @@ LSHBLOOM_API const char *lshbloom_last_error(const lshbloom *h);
  * previous read, n_out[0] / n_out[1] the number of timed K1 launches / Bloom stages; both
  * accumulators are then reset.  Either pointer may be NULL. */
 LSHBLOOM_API int lshbloom_stage_times(lshbloom *h, int32_t enable, double *ms_out, uint64_t *n_out);
+
+/* Checkpoint / resume.
+ * lshbloom_save writes the index (world = 1 handles) as SPEC's little-endian "LSHB" container:
+ *   "LSHB" | version u32 (1) | threshold f64 ((1/b)^(1/r), the S-curve midpoint; create takes b,r)
+ *   | num_perm u32 | b u32 | r u32 | signature_seed u64 | band_hash_seed u64 (both = seed)
+ *   | n_docs u64 (n_expected) | p_effective f64 (1-(1-p)^b) | doc_count u64
+ *   | b filter encodings | CRC32C u32 of every preceding byte,
+ * each filter encoding being SPEC's "LBF1" record:
+ *   "LBF1" | version u32 (1) | seed u64 (s1_j) | capacity_n u64 | target_p f64 (per-filter p)
+ *   | m u64 | k u32 | inserted u64 | payload ceil(m/8) bytes (bit i at byte i>>3, mask
+ *   1<<(i&7)) | CRC32C u32 of the preceding bytes of this record.
+ * Shingle width n is not part of SPEC's format; files are written only for n = 5.
+ * lshbloom_load reads such a file onto `device` (-1 = current) and returns a handle whose
+ * later query_insert calls continue the stream exactly where the saved one stopped.
+ * Errors: 1 usage (world > 1, n != 5, NULL), 5 format, 6 truncation, 7 checksum, 8 I/O. */
+LSHBLOOM_API int lshbloom_save(lshbloom *h, const char *path);
+LSHBLOOM_API int lshbloom_load(const char *path, int32_t device, lshbloom **out);
 
 /* Number of kernel launches the library issued since create (launch-count evidence). */
 LSHBLOOM_API uint64_t lshbloom_launch_count(const lshbloom *h);

@@ -15,7 +15,7 @@ import numpy as np
 _LIB_PATH = os.environ.get("LSHBLOOM_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
                                                            "liblshbloom.so")
 
-OK, EUSAGE, EDATA, ERUNTIME, ENOMEM = 0, 1, 2, 3, 4
+OK, EUSAGE, EDATA, ERUNTIME, ENOMEM, EFORMAT, ETRUNC, ECHECKSUM, EIO = range(9)
 
 
 class LSHBloomError(RuntimeError):
@@ -51,7 +51,8 @@ class _Info(ctypes.Structure):
 EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloom_signatures",
            "lshbloom_band_hashes", "lshbloom_band_hashes_sharded", "lshbloom_query_insert",
            "lshbloom_query_insert_bands", "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info",
-           "lshbloom_stage_times", "lshbloom_last_error", "lshbloom_launch_count")
+           "lshbloom_stage_times", "lshbloom_save", "lshbloom_load", "lshbloom_last_error",
+           "lshbloom_launch_count")
 
 
 def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
@@ -72,6 +73,8 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     lib.lshbloom_filter_copy.argtypes = [vp, u32, vp]
     lib.lshbloom_info.argtypes = [vp, ctypes.POINTER(_Info)]
     lib.lshbloom_stage_times.argtypes = [vp, i32, vp, vp]
+    lib.lshbloom_save.argtypes = [vp, ctypes.c_char_p]
+    lib.lshbloom_load.argtypes = [ctypes.c_char_p, i32, ctypes.POINTER(vp)]
     lib.lshbloom_last_error.argtypes = [vp]
     lib.lshbloom_last_error.restype = ctypes.c_char_p
     lib.lshbloom_launch_count.argtypes = [vp]
@@ -116,7 +119,7 @@ class LSHBloom:
 
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, shingle_n: int = 5, device: int | None = None, rank: int = 0, world: int = 1,
-                 sub_batch: int = 0):
+                 sub_batch: int = 0, _handle=None):
         self._lib = lib()
         if device is None:
             try:
@@ -124,16 +127,18 @@ class LSHBloom:
                 device = torch.cuda.current_device() if torch.cuda.is_available() else -1
             except Exception:
                 device = -1
-        cfg = _Config(num_perm, b, r, shingle_n, n_expected, fp_rate, seed & (2**64 - 1), device,
-                      rank, world, sub_batch)
-        h = ctypes.c_void_p()
-        rc = self._lib.lshbloom_create_ex(ctypes.byref(cfg), ctypes.byref(h))
-        if rc:
-            raise LSHBloomError(rc, self._lib.lshbloom_last_error(None).decode())
-        self._h = h
-        self.num_perm, self.b, self.r = num_perm, b, r
-        self.device = device
+        if _handle is None:
+            cfg = _Config(num_perm, b, r, shingle_n, n_expected, fp_rate, seed & (2**64 - 1), device,
+                          rank, world, sub_batch)
+            h = ctypes.c_void_p()
+            rc = self._lib.lshbloom_create_ex(ctypes.byref(cfg), ctypes.byref(h))
+            if rc:
+                raise LSHBloomError(rc, self._lib.lshbloom_last_error(None).decode())
+            _handle = h
+        self._h = _handle
         inf = self.info()
+        self.num_perm, self.b, self.r = inf["num_perm"], inf["b"], inf["r"]
+        self.device = device
         self.m, self.k = inf["m"], inf["k"]
         self.band_lo, self.band_hi = inf["band_lo"], inf["band_hi"]
 
@@ -220,6 +225,26 @@ class LSHBloom:
         self._check(self._lib.lshbloom_query_insert_bands(self._h, p, n, dev, stream or None,
                                                           self._ptr(out)))
         return out
+
+    def save(self, path: str):
+        """Checkpoint the filters and document count (SPEC's LSHB / LBF1 container)."""
+        self._check(self._lib.lshbloom_save(self._h, os.fsencode(path)))
+
+    @classmethod
+    def load(cls, path: str, device: int | None = None) -> "LSHBloom":
+        """Resume an index saved with save(); the stream continues where it stopped."""
+        if device is None:
+            try:
+                import torch
+                device = torch.cuda.current_device() if torch.cuda.is_available() else -1
+            except Exception:
+                device = -1
+        l = lib()
+        h = ctypes.c_void_p()
+        rc = l.lshbloom_load(os.fsencode(path), device, ctypes.byref(h))
+        if rc:
+            raise LSHBloomError(rc, l.lshbloom_last_error(None).decode())
+        return cls(0, 0, 0, 0, 0.0, device=device, _handle=h)
 
     def reset(self):
         self._check(self._lib.lshbloom_reset(self._h))

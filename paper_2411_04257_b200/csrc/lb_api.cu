@@ -788,3 +788,247 @@ const char* lshbloom_last_error(const lshbloom* h) { return h ? h->err.c_str() :
 uint64_t lshbloom_launch_count(const lshbloom* h) { return h ? h->launches : 0; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// Checkpoint / resume in SPEC's LSHB / LBF1 little-endian formats.
+#include <cstdio>
+#if defined(__x86_64__)
+#include <nmmintrin.h>
+#endif
+
+namespace {
+
+uint32_t crc32c_table[256];
+bool crc32c_init_done = false;
+
+void crc32c_init() {
+  if (crc32c_init_done) return;
+  for (uint32_t i = 0; i < 256; i++) {
+    uint32_t c = i;
+    for (int k = 0; k < 8; k++) c = (c >> 1) ^ (0x82F63B78u & (0u - (c & 1)));
+    crc32c_table[i] = c;
+  }
+  crc32c_init_done = true;
+}
+
+#if defined(__x86_64__)
+__attribute__((target("sse4.2"))) uint32_t crc32c_hw(uint32_t crc, const uint8_t* p, size_t n) {
+  uint64_t c = crc;
+  while (n >= 8) {
+    uint64_t v;
+    memcpy(&v, p, 8);
+    c = _mm_crc32_u64(c, v);
+    p += 8;
+    n -= 8;
+  }
+  uint32_t c32 = (uint32_t)c;
+  while (n--) c32 = _mm_crc32_u8(c32, *p++);
+  return c32;
+}
+#endif
+
+// CRC32C (Castagnoli), running form: start with crc = 0, feed chunks, result is the CRC.
+struct Crc32c {
+  uint32_t state = 0xFFFFFFFFu;
+  void update(const void* data, size_t n) {
+    const uint8_t* p = (const uint8_t*)data;
+#if defined(__x86_64__)
+    if (__builtin_cpu_supports("sse4.2")) {
+      state = crc32c_hw(state, p, n);
+      return;
+    }
+#endif
+    crc32c_init();
+    uint32_t c = state;
+    for (size_t i = 0; i < n; i++) c = crc32c_table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+    state = c;
+  }
+  uint32_t value() const { return state ^ 0xFFFFFFFFu; }
+};
+
+struct Writer {
+  FILE* f;
+  Crc32c outer, inner;
+  bool ok = true;
+  void put(const void* d, size_t n, bool in_filter) {
+    if (ok && fwrite(d, 1, n, f) != n) ok = false;
+    outer.update(d, n);
+    if (in_filter) inner.update(d, n);
+  }
+  template <class T> void put_v(T v, bool in_filter) { put(&v, sizeof v, in_filter); }
+};
+
+struct Reader {
+  FILE* f;
+  Crc32c outer, inner;
+  int err = 0;   // 0 ok, 6 truncated, 8 io
+  bool get(void* d, size_t n, bool in_filter) {
+    if (err) return false;
+    size_t got = fread(d, 1, n, f);
+    if (got != n) {
+      err = ferror(f) ? LSHBLOOM_EIO : LSHBLOOM_ETRUNC;
+      return false;
+    }
+    outer.update(d, n);
+    if (in_filter) inner.update(d, n);
+    return true;
+  }
+  template <class T> bool get_v(T& v, bool in_filter) { return get(&v, sizeof v, in_filter); }
+};
+
+constexpr size_t kIoChunk = 64ull << 20;
+
+}  // namespace
+
+extern "C" {
+
+int lshbloom_save(lshbloom* h, const char* path) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!path) return fail(h, LSHBLOOM_EUSAGE, "NULL path");
+  if (h->cfg.world != 1) return fail(h, LSHBLOOM_EUSAGE, "save needs an unsharded handle (world = 1)");
+  if (h->cfg.shingle_n != 5) return fail(h, LSHBLOOM_EUSAGE, "the LSHB format carries no shingle width; save needs n = 5");
+  DeviceGuard g(h->device);
+  LB_CUDA(h, cudaDeviceSynchronize());
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(h, LSHBLOOM_EIO, std::string("cannot open ") + path + " for writing");
+  Writer w{f};
+  const lshbloom_config& c = h->cfg;
+  const double threshold = pow(1.0 / c.b, 1.0 / c.r);
+  const double p_eff = -expm1((double)c.b * log1p(-c.fp_rate));
+  w.put("LSHB", 4, false);
+  w.put_v<uint32_t>(1, false);
+  w.put_v<double>(threshold, false);
+  w.put_v<uint32_t>(c.num_perm, false);
+  w.put_v<uint32_t>(c.b, false);
+  w.put_v<uint32_t>(c.r, false);
+  w.put_v<uint64_t>(c.seed, false);
+  w.put_v<uint64_t>(c.seed, false);
+  w.put_v<uint64_t>(c.n_expected, false);
+  w.put_v<double>(p_eff, false);
+  w.put_v<uint64_t>(h->doc_count, false);
+  const uint64_t payload = (h->m + 7) / 8;
+  std::vector<uint8_t> buf(std::min<uint64_t>(payload, kIoChunk));
+  for (uint32_t j = 0; j < c.b; j++) {
+    w.inner = Crc32c();
+    w.put("LBF1", 4, true);
+    w.put_v<uint32_t>(1, true);
+    w.put_v<uint64_t>(R(c.seed, 3, j), true);
+    w.put_v<uint64_t>(c.n_expected, true);
+    w.put_v<double>(c.fp_rate, true);
+    w.put_v<uint64_t>(h->m, true);
+    w.put_v<uint32_t>(h->k, true);
+    w.put_v<uint64_t>(h->doc_count, true);
+    const uint8_t* src = (const uint8_t*)(h->d_F + (uint64_t)j * h->W);
+    for (uint64_t off = 0; off < payload; off += buf.size()) {
+      const size_t n = (size_t)std::min<uint64_t>(buf.size(), payload - off);
+      cudaError_t e = cudaMemcpy(buf.data(), src + off, n, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) {
+        fclose(f);
+        return fail_cuda(h, e, "cudaMemcpy(filter -> host)");
+      }
+      w.put(buf.data(), n, true);
+    }
+    w.put_v<uint32_t>(w.inner.value(), false);
+  }
+  const uint32_t crc = w.outer.value();
+  w.put_v<uint32_t>(crc, false);
+  const bool ok = w.ok && fclose(f) == 0;
+  if (!ok) return fail(h, LSHBLOOM_EIO, std::string("write failed: ") + path);
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_load(const char* path, int32_t device, lshbloom** out) {
+  if (!out || !path) return fail(nullptr, LSHBLOOM_EUSAGE, "NULL path / out");
+  *out = nullptr;
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(nullptr, LSHBLOOM_EIO, std::string("cannot open ") + path);
+  Reader r{f};
+  auto bail = [&](int code, const std::string& msg, lshbloom* h) {
+    fclose(f);
+    if (h) lshbloom_destroy(h);
+    return fail(nullptr, code, msg);
+  };
+  char magic[4];
+  uint32_t version, num_perm, b, rr;
+  double threshold, p_eff;
+  uint64_t sseed, bseed, n_docs, doc_count;
+  r.get(magic, 4, false);
+  r.get_v(version, false);
+  r.get_v(threshold, false);
+  r.get_v(num_perm, false);
+  r.get_v(b, false);
+  r.get_v(rr, false);
+  r.get_v(sseed, false);
+  r.get_v(bseed, false);
+  r.get_v(n_docs, false);
+  r.get_v(p_eff, false);
+  r.get_v(doc_count, false);
+  if (r.err) return bail(r.err, "truncated LSHB header", nullptr);
+  if (memcmp(magic, "LSHB", 4) != 0) return bail(LSHBLOOM_EFORMAT, "bad magic (not an LSHB file)", nullptr);
+  if (version != 1) return bail(LSHBLOOM_EFORMAT, "unsupported LSHB version " + std::to_string(version), nullptr);
+  if (sseed != bseed) return bail(LSHBLOOM_EFORMAT, "signature and band-hash seeds differ (unsupported)", nullptr);
+  lshbloom* h = nullptr;
+  bool created = false;
+  for (uint32_t j = 0; j < b; j++) {
+    r.inner = Crc32c();
+    char fm[4];
+    uint32_t fv, k;
+    uint64_t fseed, cap, m, inserted;
+    double tp;
+    r.get(fm, 4, true);
+    r.get_v(fv, true);
+    r.get_v(fseed, true);
+    r.get_v(cap, true);
+    r.get_v(tp, true);
+    r.get_v(m, true);
+    r.get_v(k, true);
+    r.get_v(inserted, true);
+    if (r.err) return bail(r.err, "truncated LBF1 header of band " + std::to_string(j), h);
+    if (memcmp(fm, "LBF1", 4) != 0 || fv != 1) return bail(LSHBLOOM_EFORMAT, "bad LBF1 record for band " + std::to_string(j), h);
+    if (!created) {
+      lshbloom_config c;
+      memset(&c, 0, sizeof c);
+      c.num_perm = num_perm;
+      c.b = b;
+      c.r = rr;
+      c.shingle_n = 5;
+      c.n_expected = cap;
+      c.fp_rate = tp;
+      c.seed = sseed;
+      c.device = device;
+      c.world = 1;
+      int rc = lshbloom_create_ex(&c, &h);
+      if (rc) return bail(rc == LSHBLOOM_EUSAGE ? LSHBLOOM_EFORMAT : rc, "header parameters rejected: " + g_create_error, nullptr);
+      created = true;
+      if (n_docs != cap) return bail(LSHBLOOM_EFORMAT, "n_docs != capacity_n", h);
+    }
+    if (m != h->m || k != h->k || cap != h->cfg.n_expected || tp != h->cfg.fp_rate || fseed != R(sseed, 3, j))
+      return bail(LSHBLOOM_EFORMAT, "LBF1 geometry of band " + std::to_string(j) + " disagrees with its parameters", h);
+    const uint64_t payload = (m + 7) / 8;
+    std::vector<uint8_t> buf(std::min<uint64_t>(payload, kIoChunk));
+    uint8_t* dst = (uint8_t*)(h->d_F + (uint64_t)j * h->W);
+    for (uint64_t off = 0; off < payload; off += buf.size()) {
+      const size_t n = (size_t)std::min<uint64_t>(buf.size(), payload - off);
+      if (!r.get(buf.data(), n, true)) return bail(r.err, "truncated payload of band " + std::to_string(j), h);
+      cudaError_t e = cudaMemcpy(dst + off, buf.data(), n, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return bail(LSHBLOOM_ERUNTIME, std::string("cudaMemcpy: ") + cudaGetErrorString(e), h);
+    }
+    const uint32_t want = r.inner.value();
+    uint32_t stored;
+    if (!r.get_v(stored, false)) return bail(r.err, "truncated LBF1 checksum", h);
+    if (stored != want) return bail(LSHBLOOM_ECHECKSUM, "LBF1 checksum mismatch in band " + std::to_string(j), h);
+    h->doc_count = inserted;
+  }
+  if (!created) return bail(LSHBLOOM_EFORMAT, "LSHB file with b = 0", nullptr);
+  const uint32_t want = r.outer.value();
+  uint32_t stored;
+  if (!r.get_v(stored, false)) return bail(r.err, "truncated LSHB checksum", h);
+  if (stored != want) return bail(LSHBLOOM_ECHECKSUM, "LSHB checksum mismatch", h);
+  h->doc_count = doc_count;
+  fclose(f);
+  *out = h;
+  return LSHBLOOM_OK;
+}
+
+}  // extern "C"
