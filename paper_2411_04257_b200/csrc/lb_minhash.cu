@@ -19,6 +19,7 @@
 // Four 32x32->64 multiplies (the minimum for a 61x61-bit product; IMAD.WIDE issues at 1/4 rate)
 // plus ~8 ALU ops; tools/micro measured the per-opcode rates.
 #include <cstdint>
+#include <cstdlib>
 
 #include "lb_internal.h"
 
@@ -203,6 +204,214 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Screened K1.  Almost no evaluation can lower a running minimum once a document's first few
+// shingles are in (P(y < m) ~ 1/s after s shingles), and whether one can is decided by the low
+// 32 bits of S' alone: with S' = A + G'_hi + G'_lo 2^29 and y = low32(S') - 1 + q, q in [0, 4],
+//   y >= m is guaranteed  <=>  u = low32(S') - 1 lies in [m, 2^32 - 5]
+//                         <=>  w = low32(S') - (m + 1)  <=  K = 2^32 - 5 - m      (mod 2^32)
+// and low32(S') needs only low32(A) (two 32-bit IMADs: half the fmaheavy cost of IMAD.WIDE) and
+// G' (two IMAD.WIDE).  Every evaluation is screened this way; the rare candidates (w > K) are
+// queued per lane and per permutation slot in shared memory and evaluated exactly (eval_trunc)
+// when the queues are flushed (every 32-shingle chunk, or earlier when a queue nears capacity).
+// The first shingle of every document is evaluated exactly to seed m; if any m > 2^32 - 5
+// (probability ~2^-30 per document) the warp keeps evaluating that document exactly.
+// Screening against a stale (larger) m only admits more candidates, so results are exact.
+#define K1S_QCAP 16
+#ifndef LB_K1S_MINB
+#define LB_K1S_MINB 1
+#endif
+
+__device__ __forceinline__ bool screen(const PermCoef& c, const XLimbs& x, uint32_t bias, uint32_t K,
+                                       uint32_t sh29) {
+  // w = low32(S') - (m + 1) = a1 xh + a0 xl + [(b+1)_lo - (m+1)] + G'_hi + (G'_lo << 29)  (mod 2^32)
+  uint32_t w;
+  asm("{\n\t"
+      ".reg .u64 G;\n\t"
+      ".reg .u32 t, g0, g1;\n\t"
+      "mad.lo.u32 t, %1, %3, %7;\n\t"
+      "mad.lo.u32 t, %2, %4, t;\n\t"
+      "mul.wide.u32 G, %1, %5;\n\t"
+      "mad.wide.u32 G, %2, %6, G;\n\t"
+      "mov.b64 {g0, g1}, G;\n\t"
+      "shl.b32 g0, g0, %8;\n\t"          // run-time 29: keeps the shift-add off the fmaheavy pipe
+      "add.u32 t, t, g1;\n\t"
+      "add.u32 %0, t, g0;\n\t"
+      "}"
+      : "=r"(w)
+      : "r"(c.a0), "r"(c.a1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4), "r"(bias), "r"(sh29));
+  return w > K;
+}
+
+__device__ __forceinline__ void st_shared_u8(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ uint32_t ld_shared_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const MinhashParams p) {
+  __shared__ XLimbs xs[K1_WARPS][32];
+  __shared__ uint8_t qb[K1_WARPS][NPL][K1S_QCAP][32];   // [slot][lane]: conflict-free byte stores
+  __shared__ uint32_t sg[K1_WARPS][32 * NPL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (*p.err) return;
+  PermCoef c[NPL];
+#pragma unroll
+  for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
+  const uint32_t sh29 = p.sh29, sh3 = p.sh3;
+
+  for (;;) {
+    uint32_t di = 0;
+    if (lane == 0) di = atomicAdd(p.counter, 1u);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (di >= p.n_docs) break;
+    const uint32_t d = p.doc0 + di;
+    const uint64_t o0 = p.offsets[d];
+    const uint64_t L = p.offsets[d + 1] - o0;
+    const uint32_t* tk = p.tokens + (o0 - p.tok_base);
+    const uint32_t n = p.shingle_n;
+    const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;
+    const uint32_t t = L >= n ? n : (uint32_t)L;
+    const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
+
+    uint32_t mn[NPL], bias[NPL], K[NPL];
+    bool exact_mode = false;
+    for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+      const uint32_t s = s0 + lane;
+      if (s < S) {
+        uint64_t h = init;
+        for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)__ldg(tk + s + j));
+        xs[w][lane] = make_limbs(h);
+      }
+      __syncwarp();
+      const uint32_t cnt = min(32u, S - s0);
+      uint32_t j = 0;
+      if (s0 == 0) {   // seed the minima with the first shingle, exactly
+        const XLimbs x0 = xs[w][0];
+        bool big = false;
+#pragma unroll
+        for (int q = 0; q < NPL; q++) {
+          mn[q] = eval_trunc(false, c[q], x0, sh29, sh3);
+          bias[q] = c[q].bp0 - (mn[q] + 1u);
+          K[q] = 0xFFFFFFFBu - mn[q];
+          big |= mn[q] > 0xFFFFFFFBu;
+        }
+        exact_mode = __any_sync(0xffffffffu, big);
+        j = 1;
+      }
+      if (exact_mode) {
+        for (; j < cnt; j++) {
+          const XLimbs xv = xs[w][j];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_trunc(false, c[q], xv, sh29, sh3));
+        }
+      } else {
+        uint32_t rsh29;
+        asm volatile("mov.u32 %0, %1;" : "=r"(rsh29) : "r"(sh29));   // opaque register copy
+        // per-slot queue write pointers (shared-memory byte addresses, stride 32 = one slot)
+        uint32_t qp[NPL];
+        const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(&qb[w][0][0][lane]);
+#pragma unroll
+        for (int q = 0; q < NPL; q++) qp[q] = qbase + q * (K1S_QCAP * 32);
+        auto flush = [&]() {
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            const uint32_t n = (qp[q] - (qbase + q * (K1S_QCAP * 32))) >> 5;
+            const uint32_t rounds = __reduce_max_sync(0xffffffffu, n);
+            for (uint32_t i = 0; i < rounds; i++) {
+              if (i < n) {
+                const uint32_t js = ld_shared_u8(qbase + q * (K1S_QCAP * 32) + i * 32);
+                const uint32_t y = eval_trunc(false, c[q], xs[w][js], sh29, sh3);
+                if (y < mn[q]) {
+                  mn[q] = y;
+                  bias[q] = c[q].bp0 - (y + 1u);
+                  K[q] = 0xFFFFFFFBu - y;
+                }
+              }
+            }
+            qp[q] = qbase + q * (K1S_QCAP * 32);
+          }
+        };
+        for (; j + 4 <= cnt; j += 4) {       // full groups: straight-line screening
+          XLimbs xv[4];
+#pragma unroll
+          for (int u = 0; u < 4; u++) xv[u] = xs[w][j + u];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+              if (screen(c[q], xv[u], bias[q], K[q], rsh29)) {
+                st_shared_u8(qp[q], j + u);
+                qp[q] += 32;
+              }
+            }
+          }
+          bool full = false;
+#pragma unroll
+          for (int q = 0; q < NPL; q++) full |= qp[q] - (qbase + q * (K1S_QCAP * 32)) > (K1S_QCAP - 4) * 32;
+          if (__any_sync(0xffffffffu, full)) flush();
+        }
+        for (; j < cnt; j++) {               // ragged tail of the chunk
+          const XLimbs xv = xs[w][j];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            if (screen(c[q], xv, bias[q], K[q], rsh29)) {
+              st_shared_u8(qp[q], j);
+              qp[q] += 32;
+            }
+          }
+        }
+        __syncwarp();
+        flush();
+      }
+      __syncwarp();
+    }
+
+    if (p.sig_out) {
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const uint32_t pm = lane + 32 * q;
+        if (pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = mn[q];
+      }
+    }
+    if (p.bh_out) {
+#pragma unroll
+      for (int q = 0; q < NPL; q++) sg[w][lane + 32 * q] = mn[q];
+      __syncwarp();
+      for (uint32_t jb = lane; jb < p.b; jb += 32) {
+        if (p.map.ncol[jb] == 0) continue;
+        uint64_t acc = 0;                               // BH_j, P:207-208 (DESIGN R6/R7)
+        for (uint32_t u = 0; u < p.r; u++) {
+          acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][jb * p.r + u], __ldg(p.bcoef + p.r + u));
+          acc = acc >= kP ? acc - kP : acc;
+        }
+        p.bh_out[p.map.blockstart[jb] + (uint64_t)d * p.map.ncol[jb] + p.map.col[jb]] = acc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int NPL>
+static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash_scr<NPL>, K1_THREADS, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
+  const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
+  uint64_t grid = (uint64_t)sm_count * bps;
+  if (want < grid) grid = want ? want : 1;
+  k1_minhash_scr<NPL><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  return 1;
+}
+
 template <int NPL, int UNR>
 static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
@@ -219,6 +428,24 @@ static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int ma
 }
 
 int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps) {
+  // Kernel choice (measured on B200, tools/k1_variants.py): with 128 permutations (npl 4) the
+  // exact kernel wins on abstract-length documents (C2: 1203 vs ~1100 Geval/s); with 256
+  // (npl 8) the screened kernel wins by 1.7x on full-text lengths (C3: 1489 vs 860 Geval/s).
+  // LSHBLOOM_K1=exact|screened overrides.
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("LSHBLOOM_K1");
+    mode = !e ? 2 : (e[0] == 'e' ? 0 : 1);
+  }
+  const bool screened = mode == 1 || (mode == 2 && npl >= 8);
+  if (screened && npl <= 8) {
+    switch (npl) {
+      case 1: return launch_s<1>(p, sm_count, s, max_bps);
+      case 2: return launch_s<2>(p, sm_count, s, max_bps);
+      case 4: return launch_s<4>(p, sm_count, s, max_bps);
+      case 8: return launch_s<8>(p, sm_count, s, max_bps);
+    }
+  }
   switch (npl) {
     case 1: return launch_t<1, 4>(p, sm_count, s, max_bps);
     case 2: return launch_t<2, 4>(p, sm_count, s, max_bps);

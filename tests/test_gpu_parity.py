@@ -285,3 +285,30 @@ def test_many_chunks_short_docs(on_device):
     args = to_dev(off, tok) if on_device else (off, tok)
     assert (u8(idx.query_insert(*args)) == dup).all()
     assert (u64(idx.band_hashes(*args)) == bh).all()
+
+
+@pytest.mark.parametrize("mode", ["exact", "screened"])
+def test_both_minhash_kernels(mode):
+    # run in a subprocess: the kernel choice is read once per process from LSHBLOOM_K1
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle
+from synthetic.corpus import CONFIGS, gen_range
+from paper_2411_04257_b200 import LSHBloom
+for name, n in (("C1", 3000), ("C3", 300)):
+    cfg = CONFIGS[name]
+    off, tok = gen_range(cfg, 0, n)
+    sig, bh, dup, _ = oracle.run(off, tok, num_perm=cfg.num_perm, b=cfg.b, r=cfg.r, n_expected=n,
+                                 fp_rate=cfg.fp_rate, seed=cfg.seed)
+    idx = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n, cfg.fp_rate, cfg.seed, device=0)
+    d = (torch.from_numpy(off.view(np.int64)).cuda(), torch.from_numpy(tok.view(np.int32)).cuda())
+    assert (idx.signatures(*d).cpu().numpy().view(np.uint32) == sig).all(), name
+    assert (idx.query_insert(*d).cpu().numpy() == dup).all(), name
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LSHBLOOM_K1=mode, PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

@@ -26,14 +26,14 @@ def build(specs):
         print("built", out, flags)
 
 
-def one(path, docs, reps):
+def one(path, docs, reps, config="C2"):
     import numpy as np
     import torch
     os.environ["LSHBLOOM_LIB"] = path
     from paper_2411_04257_b200 import LSHBloom
     from synthetic.corpus import CONFIGS, gen_range
-    cfg = CONFIGS["C2"]
-    cache = "/tmp/c2_%d.npz" % docs
+    cfg = CONFIGS[config]
+    cache = "/tmp/%s_%d.npz" % (config, docs)
     if os.path.exists(cache):
         z = np.load(cache)
         off, tok = z["off"], z["tok"]
@@ -73,6 +73,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "build":
         build(sys.argv[2:])
     elif sys.argv[1] == "one":
-        print(json.dumps(one(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))))
+        print(json.dumps(one(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]),
+                             sys.argv[5] if len(sys.argv) > 5 else "C2")))
     else:
         run(int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000)
