@@ -61,7 +61,7 @@ struct lshbloom {
   uint64_t* d_s2 = nullptr;
   uint32_t* d_F = nullptr;
   uint64_t* d_Q = nullptr;        // 2 compact earliest-setter tables of 2^q_log2 slots
-  uint32_t q_log2 = 20;
+  uint32_t q_log2 = 19;
   uint64_t* d_ekey = nullptr;
   uint64_t* d_eval = nullptr;
   uint32_t ecap_log2 = 0;
@@ -199,12 +199,16 @@ BandMap sharded_map(const lshbloom* h, uint64_t n) {
   return m;
 }
 
-BandMap owned_map(const lshbloom* h) {
+
+// Band-major [b_local][n] layout for the fused query_insert path (the Bloom kernels walk one
+// band's filter at a time).
+BandMap owned_band_major_map(const lshbloom* h, uint64_t n) {
   BandMap m;
   memset(&m, 0, sizeof m);
   for (uint32_t j = h->band_lo; j < h->band_hi; j++) {
-    m.ncol[j] = h->bl;
-    m.col[j] = j - h->band_lo;
+    m.blockstart[j] = (uint64_t)(j - h->band_lo) * n;
+    m.ncol[j] = 1;
+    m.col[j] = 0;
   }
   return m;
 }
@@ -326,8 +330,8 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
 }
 
 // K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
-int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_end, uint8_t* dup_dev,
-              cudaStream_t s, bool first = true, bool last = true) {
+int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin, uint64_t i_end,
+              uint8_t* dup_dev, cudaStream_t s, bool first = true, bool last = true) {
   BloomParams p;
   memset(&p, 0, sizeof p);
   p.F = h->d_F;
@@ -343,6 +347,8 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t i_begin, uint64_t i_
   p.eval = h->d_eval;
   p.ecap_log2 = h->ecap_log2;
   p.bh = bh_dev;
+  p.bh_sj = bh_sj;
+  p.bh_si = bh_si;
   const uint64_t SB = h->sub_batch;
   p.st_pre = h->d_st;
   p.st_arr = h->d_st + SB * h->bl;
@@ -391,7 +397,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   uint64_t* bh = (uint64_t*)h->bh.p;
   MinhashParams p = base_params(h);
   p.bh_out = bh;
-  p.map = owned_map(h);
+  p.map = owned_band_major_map(h, n);
   int rc = reset_err(h, s);
   if (rc) return rc;
   uint64_t chunk_tokens = 0;
@@ -440,7 +446,6 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     }
     p.doc0 = (uint32_t)d0;
     p.n_docs = (uint32_t)(d1 - d0);
-    p.map = owned_map(h);
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
     int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
@@ -450,7 +455,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     if (d1 == n) stage_end(h, 0, s);
     LB_CUDA(h, cudaEventRecord(h->ev_fuse, s));
     LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
-    if ((rc = run_bloom(h, bh, d0, d1, ddup, h->bloom_stream, d0 == 0, d1 == n))) return rc;
+    if ((rc = run_bloom(h, bh, n, 1, d0, d1, ddup, h->bloom_stream, d0 == 0, d1 == n))) return rc;
     d0 = d1;
     c++;
   }
@@ -544,7 +549,13 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev));
   CR(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
   CR(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
-  CR(cudaStreamCreateWithFlags(&h->bloom_stream, cudaStreamNonBlocking));
+  {
+    // the latency-bound Bloom kernels get priority over K1 for SM slots as blocks retire
+    int lo = 0, hi = 0;
+    CR(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (const char* e = getenv("LSHBLOOM_BLOOM_PRIO")) hi = atoi(e) ? hi : lo;
+    CR(cudaStreamCreateWithPriority(&h->bloom_stream, cudaStreamNonBlocking, hi));
+  }
   CR(cudaEventCreateWithFlags(&h->ev_fuse, cudaEventDisableTiming));
   h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
   if (const char* e = getenv("LSHBLOOM_K1_BPS")) h->k1_bps = atoi(e);
@@ -734,7 +745,7 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   }
   if ((rc = reset_err(h, s))) return rc;
   LB_CUDA(h, cudaMemsetAsync(dhit, 0, n_docs, s));
-  if ((rc = run_bloom(h, dbh, 0, n_docs, dhit, s))) return rc;
+  if ((rc = run_bloom(h, dbh, 1, h->bl, 0, n_docs, dhit, s))) return rc;
   if (!on_device) LB_CUDA(h, cudaMemcpyAsync(hit_out, dhit, n_docs, cudaMemcpyDeviceToHost, s));
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n_docs;

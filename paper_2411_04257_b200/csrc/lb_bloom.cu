@@ -165,9 +165,9 @@ template <int KT>
 __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
-  const uint32_t jl = (uint32_t)(idx % p.bl);
-  const uint32_t i = p.i0 + (uint32_t)(idx / p.bl);
-  const uint64_t bh = p.bh[(uint64_t)i * p.bl + jl];
+  const uint32_t jl = (uint32_t)(idx / p.nsb);          // band-major: a wave touches few filters
+  const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
+  const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
   uint64_t pre = 0;
   if constexpr (KT > 0) {
@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
   const uint64_t pre = p.st_pre[idx];
   if (pre == full_mask(p.k)) return;
-  const uint32_t jl = (uint32_t)(idx % p.bl);
-  const uint32_t i = p.i0 + (uint32_t)(idx / p.bl);
-  const uint64_t bh = p.bh[(uint64_t)i * p.bl + jl];
+  const uint32_t jl = (uint32_t)(idx / p.nsb);          // band-major: a wave touches few filters
+  const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
+  const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   uint32_t* F = p.F + (uint64_t)jl * p.W;
   uint64_t arr = 0;
   auto settle = [&](uint32_t t, uint64_t g, uint32_t old) {
@@ -235,11 +235,11 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   const uint64_t pre = p.st_pre[idx];
   if (pre == full_mask(p.k)) return;
   const uint64_t arr = p.st_arr[idx];
-  const uint32_t jl = (uint32_t)(idx % p.bl);
-  const uint32_t i = p.i0 + (uint32_t)(idx / p.bl);
+  const uint32_t jl = (uint32_t)(idx / p.nsb);
+  const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
   bool maybe = true;
   if (arr) {
-    const uint64_t bh = p.bh[(uint64_t)i * p.bl + jl];
+    const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
     // (not early-exiting: every contested first arrival must join E for the other docs)
     ProbeGen gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
@@ -262,10 +262,10 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += stride) {
     const uint32_t idx = p.cand[c];
-    const uint32_t jl = idx % p.bl;
-    const uint32_t i = p.i0 + idx / p.bl;
+    const uint32_t jl = idx / p.nsb;
+    const uint32_t i = p.i0 + idx % p.nsb;
     const uint64_t pre = p.st_pre[idx];
-    ProbeGen gen(p, p.bh[(uint64_t)i * p.bl + jl], jl);
+    ProbeGen gen(p, p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si], jl);
     bool hit = true;
     for (uint32_t t = 0; t < p.k && hit; t++) {
       const uint64_t g = gen.next();

@@ -51,8 +51,9 @@ struct BloomParams {
   uint64_t* eval;
   uint32_t ecap_log2;
   uint64_t gen;              // sub-batch generation tag (1 .. 2^22-1)
-  const uint64_t* bh;        // [n][bl] band hashes of the batch
-  uint32_t i0, nsb;          // sub-batch = batch documents [i0, i0 + nsb)
+  const uint64_t* bh;        // band hashes of the batch: owned band jl of doc i at bh[jl*bh_sj + i*bh_si]
+  uint64_t bh_sj, bh_si;     //   ([bl][n] band-major from K1: (n, 1); [n][bl] row-major: (1, bl))
+  uint32_t i0, nsb;          // sub-batch = batch documents [i0, i0 + nsb); thread idx = jl * nsb + (i - i0)
   uint64_t* st_pre;          // [nsb * bl] per (doc, band): pre-set probe mask (K3)
   uint64_t* st_arr;          //   and first-arrival probe mask (K4)
   uint32_t* cand;            // candidate (doc, band) pairs
