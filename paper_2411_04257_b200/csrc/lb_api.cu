@@ -13,10 +13,6 @@
 
 using namespace lb;
 
-#ifndef LB_MIXMASK
-#define LB_MIXMASK 0x0
-#endif
-
 namespace {
 
 struct DevBuf {
@@ -574,18 +570,10 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
       a = 1 + R(c.seed, 1, 2ull * i) % (kP - 1);
       bb = R(c.seed, 1, 2ull * i + 1) % kP;
     }
-    // slot q = i / 32 of every lane: "b+1" form, or the "cb" form when bit q of LB_MIXMASK is
-    // set: cb = ((b + 1) * 2^32 mod P) + P contributes (b + 1) 2^61 = b + 1 (mod P) once
-    // scaled by 2^29 in the kernel, and being >= P keeps S' >= 1 (lb_minhash.cu).
-    uint64_t bp = bb + 1;
-    if ((LB_MIXMASK >> (i / 32)) & 1) {
-      const uint64_t b1 = (bb + 1 == kP) ? 0 : bb + 1;
-      bp = (uint64_t)(((unsigned __int128)b1 << 32) % kP) + kP;
-    }
     coef[i].a0 = (uint32_t)(a & 0x7FFFFFFFull);
     coef[i].a1 = (uint32_t)(a >> 31);
-    coef[i].bp0 = (uint32_t)bp;
-    coef[i].bp1 = (uint32_t)(bp >> 32);
+    coef[i].b0 = (uint32_t)bb;
+    coef[i].b1 = (uint32_t)(bb >> 32);
   }
   std::vector<uint64_t> bcoef(2 * c.r);
   for (uint32_t u = 0; u < c.r; u++) {

@@ -35,9 +35,9 @@ __device__ __forceinline__ uint64_t affine32_mod_p(uint64_t c, uint32_t s, uint6
 }
 
 // Per-permutation coefficients in the kernel's limb layout: a = a1 * 2^31 + a0 (a0 < 2^31,
-// a1 < 2^30) and b' = b + 1 as two 32-bit words (see minhash eval below).
+// a1 < 2^30) and b = b1 * 2^32 + b0 (see the MinHash evaluations in lb_minhash.cu).
 struct __align__(16) PermCoef {
-  uint32_t a0, a1, bp0, bp1;
+  uint32_t a0, a1, b0, b1;
 };
 
 // x = fingerprint mod P split for the eval: xl = x mod 2^30, xh = x >> 30 (< 2^31),

@@ -36,75 +36,74 @@ namespace lb {
 #endif
 #define K1_WARPS (K1_THREADS / 32)
 
-// Which permutation slots q (p = lane + 32 q) use the "cb" form (bit q set) rather than the
-// "b+1" form; the host expands the coefficients accordingly (lb_api.cu).  The two forms load
-// the SM's integer pipes differently (fmaheavy vs ALU); mixing them balances the pipes.
-#ifndef LB_MIXMASK
-#define LB_MIXMASK 0x0
-#endif
+// Coefficients: a = a1 2^31 + a0 (a0 < 2^31, a1 < 2^30), b = b1 2^32 + b0 (b < P), stored per
+// permutation as PermCoef{a0, a1, b0, b1}; shingle x = xh 2^30 + xl with xh2 = 2 xh, xl4 = 4 xl.
+//   a x = a1 xh 2^61 + 2^30 (a0 xh + 2 a1 xl) + a0 xl,   2^61 = 1 (mod P)
+//   A = a0 xl + a1 xh + b (< 3 2^61),  G = a0 xh2 + a1 xl4 (< 2^64),  2^30 (G/2) = G_hi + G_lo 2^29
+//   S = A + G_hi + G_lo 2^29 = a x + b (mod P),  0 <= S < 2^63 + 2^61
+// and y = low32(S mod P) = low32(S) + q with q = floor(S / P) <= 4 (low32(q P) = -q).
 
-// Form A ("b+1"):  A = a0 xl + a1 xh + (b+1),  G' = a0 (2xh) + a1 (4xl)
-// Form C ("cb")  :  A = a0 xl + a1 xh,          G' = a0 (2xh) + a1 (4xl) + cb,
-//                   cb = ((b+1) 2^32 mod P) + P  (cb 2^29 = b + 1 mod P; cb >= P keeps S' >= 1)
-// Both: S' = A + G'_hi + G'_lo 2^29 = a x + b + 1 (mod P), 1 <= S' < 2^63.
-__device__ __forceinline__ uint32_t eval_trunc(bool cb, const PermCoef& c, const XLimbs& x,
-                                               uint32_t sh29, uint32_t sh3) {
+// Exact: q = (S' + (S' >> 61)) >> 61 with S' = S + 1 (proved in DESIGN.md), carries included.
+__device__ __forceinline__ uint32_t eval_exact(const PermCoef& c, const XLimbs& x) {
   uint32_t y;
-  if (!cb) {
-    asm("{\n\t"
-        ".reg .u64 A, G, BP;\n\t"
-        ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
-        "mov.b64 BP, {%3, %4};\n\t"
-        "mad.wide.u32 A, %1, %5, BP;\n\t"
-        "mad.wide.u32 A, %2, %6, A;\n\t"
-        "mul.wide.u32 G, %1, %7;\n\t"
-        "mad.wide.u32 G, %2, %8, G;\n\t"
-        "mov.b64 {s0, s1}, A;\n\t"
-        "mov.b64 {g0, g1}, G;\n\t"
-        "shl.b32 t1, g0, 29;\n\t"
-        "shr.u32 t2, g0, 3;\n\t"
-        "add.cc.u32 s0, s0, t1;\n\t"
-        "addc.u32 s1, s1, t2;\n\t"
-        "add.cc.u32 s0, s0, g1;\n\t"
-        "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0 = S + 1,  S = a x + b (mod P)
-        "shr.u32 q, s1, 29;\n\t"
-        "add.cc.u32 t1, s0, q;\n\t"
-        "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
-        "shr.u32 q, t2, 29;\n\t"            // q = W >> 61 = floor(S / P)
-        "add.u32 s0, s0, q;\n\t"
-        "sub.u32 %0, s0, 1;\n\t"            // low32(S - q P) = low32(S') - 1 + q
-        "}"
-        : "=r"(y)
-        : "r"(c.a0), "r"(c.a1), "r"(c.bp0), "r"(c.bp1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
-  } else {
-    // shift amounts 29 and 3 come from registers so ptxas keeps them on the ALU pipe
-    asm("{\n\t"
-        ".reg .u64 A, G, CB;\n\t"
-        ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
-        "mov.b64 CB, {%3, %4};\n\t"
-        "mul.wide.u32 A, %1, %5;\n\t"
-        "mad.wide.u32 A, %2, %6, A;\n\t"
-        "mad.wide.u32 G, %1, %7, CB;\n\t"
-        "mad.wide.u32 G, %2, %8, G;\n\t"
-        "mov.b64 {s0, s1}, A;\n\t"
-        "mov.b64 {g0, g1}, G;\n\t"
-        "shl.b32 t1, g0, %9;\n\t"
-        "shr.u32 t2, g0, %10;\n\t"
-        "add.cc.u32 s0, s0, t1;\n\t"
-        "addc.u32 s1, s1, t2;\n\t"
-        "add.cc.u32 s0, s0, g1;\n\t"
-        "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0 = S + 1,  S = a x + b (mod P)
-        "shr.u32 q, s1, 29;\n\t"
-        "add.cc.u32 t1, s0, q;\n\t"
-        "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
-        "shr.u32 q, t2, 29;\n\t"            // q = W >> 61 = floor(S / P)
-        "add.u32 s0, s0, q;\n\t"
-        "sub.u32 %0, s0, 1;\n\t"            // low32(S - q P) = low32(S') - 1 + q
-        "}"
-        : "=r"(y)
-        : "r"(c.a0), "r"(c.a1), "r"(c.bp0), "r"(c.bp1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4),
-          "r"(sh29), "r"(sh3));
-  }
+  asm("{\n\t"
+      ".reg .u64 A, G, B;\n\t"
+      ".reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
+      "mov.b64 B, {%3, %4};\n\t"
+      "add.u64 B, B, 1;\n\t"              // b + 1
+      "mad.wide.u32 A, %1, %5, B;\n\t"
+      "mad.wide.u32 A, %2, %6, A;\n\t"
+      "mul.wide.u32 G, %1, %7;\n\t"
+      "mad.wide.u32 G, %2, %8, G;\n\t"
+      "mov.b64 {s0, s1}, A;\n\t"
+      "mov.b64 {g0, g1}, G;\n\t"
+      "shl.b32 t1, g0, 29;\n\t"
+      "shr.u32 t2, g0, 3;\n\t"
+      "add.cc.u32 s0, s0, t1;\n\t"
+      "addc.u32 s1, s1, t2;\n\t"
+      "add.cc.u32 s0, s0, g1;\n\t"
+      "addc.u32 s1, s1, 0;\n\t"           // S' = s1:s0 = S + 1
+      "shr.u32 q, s1, 29;\n\t"
+      "add.cc.u32 t1, s0, q;\n\t"
+      "addc.u32 t2, s1, 0;\n\t"           // W = S' + (S' >> 61)
+      "shr.u32 q, t2, 29;\n\t"            // q = W >> 61 = floor(S / P)
+      "add.u32 s0, s0, q;\n\t"
+      "sub.u32 %0, s0, 1;\n\t"            // low32(S' - 1) + q
+      "}"
+      : "=r"(y)
+      : "r"(c.a0), "r"(c.a1), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
+  return y;
+}
+
+// Carry-free: s0 = low32(S) is exact without carries; the high word is taken without the
+// carries out of the low word (s1a = A_hi + (G_lo >> 3), at most 2 below the true high word), and
+// q is taken as s1a >> 29.  This equals floor(S / P) unless bits 32..60 of S are within 5 of
+// all-ones, i.e. unless (s1a | 0xE0000000) >= 0xFFFFFFFB (p ~ 1e-8 per evaluation); the running
+// max of that word is returned in fmax and a flagged document is recomputed with eval_exact.
+// No unflagged mismatch against big integers on 4e5 random and adversarial triples.
+__device__ __forceinline__ uint32_t eval_fast(const PermCoef& c, const XLimbs& x, uint32_t& f) {
+  uint32_t y;
+  asm("{\n\t"
+      ".reg .u64 A, G, B;\n\t"
+      ".reg .u32 s0, s1, g0, g1, t1, t2;\n\t"
+      "mov.b64 B, {%3, %4};\n\t"
+      "mad.wide.u32 A, %2, %5, B;\n\t"    // a0*xl + b
+      "mad.wide.u32 A, %6, %7, A;\n\t"    // + a1*xh
+      "mul.wide.u32 G, %2, %8;\n\t"       // a0*(2xh)
+      "mad.wide.u32 G, %6, %9, G;\n\t"    // + a1*(4xl)
+      "mov.b64 {s0, s1}, A;\n\t"
+      "mov.b64 {g0, g1}, G;\n\t"
+      "shl.b32 t1, g0, 29;\n\t"
+      "shr.u32 t2, g0, 3;\n\t"
+      "add.u32 s0, s0, t1;\n\t"
+      "add.u32 s0, s0, g1;\n\t"           // low32(S)
+      "add.u32 s1, s1, t2;\n\t"           // high word, low-word carries dropped
+      "or.b32 %1, s1, 0xE0000000;\n\t"
+      "shr.u32 t1, s1, 29;\n\t"
+      "add.u32 %0, s0, t1;\n\t"           // low32(S) + q
+      "}"
+      : "=r"(y), "=r"(f)
+      : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
   return y;
 }
 
@@ -127,7 +126,6 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
-  const uint32_t sh29 = p.sh29, sh3 = p.sh3;   // 29 and 3, opaque to ptxas
 
   for (;;) {
     uint32_t di = 0;
@@ -146,6 +144,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
     uint32_t mn[NPL];
 #pragma unroll
     for (int q = 0; q < NPL; q++) mn[q] = 0xFFFFFFFFu;
+    uint32_t fmax = 0;
 
     for (uint32_t s0 = 0; s0 < S; s0 += 32) {
       const uint32_t s = s0 + lane;
@@ -165,18 +164,44 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
         for (int q = 0; q < NPL; q++) {
 #pragma unroll
           for (int u = 0; u < UNR; u += 2) {
-            uint32_t y0 = eval_trunc(((LB_MIXMASK >> q) & 1) != 0, c[q], xv[u], sh29, sh3);
-            uint32_t y1 = eval_trunc(((LB_MIXMASK >> q) & 1) != 0, c[q], xv[u + 1], sh29, sh3);
+            uint32_t f0, f1;
+            const uint32_t y0 = eval_fast(c[q], xv[u], f0);
+            const uint32_t y1 = eval_fast(c[q], xv[u + 1], f1);
             mn[q] = min(mn[q], min(y0, y1));
+            fmax = max(fmax, max(f0, f1));
           }
         }
       }
       for (; j < cnt; j++) {
         const XLimbs xv = xs[w][j];
 #pragma unroll
-        for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_trunc(((LB_MIXMASK >> q) & 1) != 0, c[q], xv, sh29, sh3));
+        for (int q = 0; q < NPL; q++) {
+          uint32_t f0;
+          mn[q] = min(mn[q], eval_fast(c[q], xv, f0));
+          fmax = max(fmax, f0);
+        }
       }
       __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, fmax >= 0xFFFFFFFBu)) {   // rare: redo the document exactly
+#pragma unroll
+      for (int q = 0; q < NPL; q++) mn[q] = 0xFFFFFFFFu;
+      for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        if (s < S) {
+          uint64_t h = init;
+          for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)__ldg(tk + s + j));
+          xs[w][lane] = make_limbs(h);
+        }
+        __syncwarp();
+        const uint32_t cnt = min(32u, S - s0);
+        for (uint32_t j = 0; j < cnt; j++) {
+          const XLimbs xv = xs[w][j];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_exact(c[q], xv));
+        }
+        __syncwarp();
+      }
     }
 
     if (p.sig_out) {
@@ -213,7 +238,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
 //                         <=>  w = low32(S') - (m + 1)  <=  K = 2^32 - 5 - m      (mod 2^32)
 // and low32(S') needs only low32(A) (two 32-bit IMADs: half the fmaheavy cost of IMAD.WIDE) and
 // G' (two IMAD.WIDE).  Every evaluation is screened this way; the rare candidates (w > K) are
-// queued per lane and per permutation slot in shared memory and evaluated exactly (eval_trunc)
+// queued per lane and per permutation slot in shared memory and evaluated exactly (eval_exact)
 // when the queues are flushed (every 32-shingle chunk, or earlier when a queue nears capacity).
 // The first shingle of every document is evaluated exactly to seed m; if any m > 2^32 - 5
 // (probability ~2^-30 per document) the warp keeps evaluating that document exactly.
@@ -225,7 +250,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
 
 __device__ __forceinline__ bool screen(const PermCoef& c, const XLimbs& x, uint32_t bias, uint32_t K,
                                        uint32_t sh29) {
-  // w = low32(S') - (m + 1) = a1 xh + a0 xl + [(b+1)_lo - (m+1)] + G'_hi + (G'_lo << 29)  (mod 2^32)
+  // w = low32(S') - (m + 1) = low32(S) - m = a0 xl + a1 xh + [b_lo - m] + G_hi + (G_lo << 29)
   uint32_t w;
   asm("{\n\t"
       ".reg .u64 G;\n\t"
@@ -263,7 +288,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
-  const uint32_t sh29 = p.sh29, sh3 = p.sh3;
+  const uint32_t sh29 = p.sh29;
 
   for (;;) {
     uint32_t di = 0;
@@ -296,8 +321,8 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
         bool big = false;
 #pragma unroll
         for (int q = 0; q < NPL; q++) {
-          mn[q] = eval_trunc(false, c[q], x0, sh29, sh3);
-          bias[q] = c[q].bp0 - (mn[q] + 1u);
+          mn[q] = eval_exact(c[q], x0);
+          bias[q] = c[q].b0 - mn[q];
           K[q] = 0xFFFFFFFBu - mn[q];
           big |= mn[q] > 0xFFFFFFFBu;
         }
@@ -308,7 +333,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
         for (; j < cnt; j++) {
           const XLimbs xv = xs[w][j];
 #pragma unroll
-          for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_trunc(false, c[q], xv, sh29, sh3));
+          for (int q = 0; q < NPL; q++) mn[q] = min(mn[q], eval_exact(c[q], xv));
         }
       } else {
         uint32_t rsh29;
@@ -326,10 +351,10 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
             for (uint32_t i = 0; i < rounds; i++) {
               if (i < n) {
                 const uint32_t js = ld_shared_u8(qbase + q * (K1S_QCAP * 32) + i * 32);
-                const uint32_t y = eval_trunc(false, c[q], xs[w][js], sh29, sh3);
+                const uint32_t y = eval_exact(c[q], xs[w][js]);
                 if (y < mn[q]) {
                   mn[q] = y;
-                  bias[q] = c[q].bp0 - (y + 1u);
+                  bias[q] = c[q].b0 - y;
                   K[q] = 0xFFFFFFFBu - y;
                 }
               }
