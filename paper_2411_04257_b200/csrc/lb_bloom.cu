@@ -81,10 +81,12 @@ __device__ uint32_t e_lookup(const BloomParams& p, uint64_t key) {
 
 // K4: enter doc i as a setter of contested key (earliest wins).
 __device__ void e_add(const BloomParams& p, uint64_t key, uint32_t i) {
+  LB_ASSERT(i >= p.i0 && i - p.i0 < (1u << 22) && key < (1ull << 42));
   const uint64_t packed = (key << 22) | (uint64_t)(i - p.i0);
   const uint64_t mask = (1ull << p.q_log2) - 1;
   uint64_t s = qslot(p, key);
   for (int n = 0; n < kQProbe; n++, s = (s + 1) & mask) {
+    LB_ASSERT(s <= mask);
     uint64_t cur = __ldcg(p.Q + s);
     if (cur == kQEmpty) {
       cur = atomicCAS((unsigned long long*)(p.Q + s), (unsigned long long)kQEmpty, (unsigned long long)packed);
@@ -142,6 +144,7 @@ struct ProbeGen {   // sequential positions (any k)
   }
   __device__ __forceinline__ uint64_t next() {
     const uint64_t g = x;
+    LB_ASSERT(g < m);
     x += dl;
     x = x >= m ? x - m : x;
     return g;
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
   const uint32_t jl = (uint32_t)(idx / p.nsb);          // band-major: a wave touches few filters
   const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
+  LB_ASSERT(jl < p.bl);
   const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
   uint64_t pre = 0;
@@ -197,6 +201,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   if (pre == full_mask(p.k)) return;
   const uint32_t jl = (uint32_t)(idx / p.nsb);          // band-major: a wave touches few filters
   const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
+  LB_ASSERT(jl < p.bl);
   const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   uint32_t* F = p.F + (uint64_t)jl * p.W;
   uint64_t arr = 0;
@@ -262,6 +267,7 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += stride) {
     const uint32_t idx = p.cand[c];
+    LB_ASSERT(idx < (uint64_t)p.nsb * p.bl);
     const uint32_t jl = idx / p.nsb;
     const uint32_t i = p.i0 + idx % p.nsb;
     const uint64_t pre = p.st_pre[idx];

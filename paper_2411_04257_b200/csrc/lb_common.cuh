@@ -3,8 +3,18 @@
 // Independent implementation of the conventions in DESIGN.md section 3; shares no code
 // with oracle/ (the CPU oracle re-implements every step for parity testing).
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+// Bounds / invariant checks for a debug build (-DLB_CHECKS): compute-sanitizer is not
+// available on the B200 pool, so tests/test_gpu_checked.py reruns parity cases against a
+// library built with these device asserts.
+#ifdef LB_CHECKS
+#define LB_ASSERT(x) assert(x)
+#else
+#define LB_ASSERT(x) ((void)0)
+#endif
 
 namespace lb {
 

@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
     const uint32_t d = p.doc0 + di;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
+    LB_ASSERT(L >= 1 && o0 >= p.tok_base);
     const uint32_t* tk = p.tokens + (o0 - p.tok_base);
     const uint32_t n = p.shingle_n;
     const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;     // the bag of n-grams
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
     const uint32_t d = p.doc0 + di;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
+    LB_ASSERT(L >= 1 && o0 >= p.tok_base);
     const uint32_t* tk = p.tokens + (o0 - p.tok_base);
     const uint32_t n = p.shingle_n;
     const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
 #pragma unroll
             for (int u = 0; u < 4; u++) {
               if (screen(c[q], xv[u], bias[q], K[q], rsh29)) {
+                LB_ASSERT(qp[q] < qbase + (q + 1) * (K1S_QCAP * 32));
                 st_shared_u8(qp[q], j + u);
                 qp[q] += 32;
               }
@@ -386,6 +389,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
 #pragma unroll
           for (int q = 0; q < NPL; q++) {
             if (screen(c[q], xv, bias[q], K[q], rsh29)) {
+              LB_ASSERT(qp[q] < qbase + (q + 1) * (K1S_QCAP * 32));
               st_shared_u8(qp[q], j);
               qp[q] += 32;
             }
