@@ -13,8 +13,8 @@
 //   K5 resolve : each first arrival looks its position up in E: if present (contested) it joins
 //                the minimum; if absent it is the position's sole prober, so its band misses
 //                (E[p] = i).  Bands whose every pre-unset probe is contested become candidates.
-//   K6 verdict : candidate hit <=> E[p] < i for every pre-unset probe p; then clear the
-//                previous sub-batch's E buffer.
+//   K6 verdict : candidate hit <=> E[p] < i for every pre-unset probe p.  (The previous
+//                sub-batch's E buffer is reset by a memset queued before K3.)
 // E holds only contested positions.  Its primary form Q is a compact open-addressed table of
 // packed u64 slots ((band, position) << 22 | doc - i0; atomicMin keeps the earliest doc), two
 // buffers alternating by sub-batch, small enough to stay L2-resident.  A key whose probe
@@ -151,20 +151,20 @@ struct ProbeGen {   // sequential positions (any k)
   }
 };
 
-template <int KT>   // KT > 0: all k positions in registers
+template <int KT, typename PT>   // KT > 0: all k positions in registers (PT = u32 when m <= 2^32)
 struct Probes {
-  uint64_t g[KT];
+  PT g[KT];
   __device__ __forceinline__ Probes(const BloomParams& p, uint64_t bh, uint32_t jl) {
     ProbeGen gen(p, bh, jl);
 #pragma unroll
-    for (int t = 0; t < KT; t++) g[t] = gen.next();
+    for (int t = 0; t < KT; t++) g[t] = (PT)gen.next();
   }
 };
 
 __device__ __forceinline__ uint64_t full_mask(uint32_t k) { return k == 64 ? ~0ull : ((1ull << k) - 1); }
 
 // K3: probe positions + pre-sub-batch test.
-template <int KT>
+template <int KT, typename PT>
 __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
   uint64_t pre = 0;
   if constexpr (KT > 0) {
-    const Probes<KT> pr(p, bh, jl);
+    const Probes<KT, PT> pr(p, bh, jl);
     uint32_t w[KT];
 #pragma unroll
     for (int t = 0; t < KT; t++) w[t] = __ldcg(F + (pr.g[t] >> 5));   // all loads in flight
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
 }
 
 // K4: insert pre-unset probes; detect contested positions.
-template <int KT>
+template <int KT, typename PT>
 __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
     }
   };
   if constexpr (KT > 0) {
-    const Probes<KT> pr(p, bh, jl);
+    const Probes<KT, PT> pr(p, bh, jl);
     uint32_t old[KT];
 #pragma unroll
     for (int t = 0; t < KT; t++)         // all atomics in flight before any result is used
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
 }
 
 // K5: first arrivals consult C; contested ones join E; sole probers make the band miss.
-template <int KT>
+template <int KT, typename PT>
 __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   }
 }
 
-// K6: verdict for candidate (doc, band) pairs; then zero the previous sub-batch's C buffer.
-template <int KT>
+// K6: verdict for candidate (doc, band) pairs.
+template <int KT, typename PT>
 __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
   if (*p.err) return;
   const uint32_t nc = *p.cand_count;
@@ -279,24 +279,28 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
     }
     if (hit) p.dup[i] = 1;
   }
-  const uint64_t slots = 1ull << p.q_log2;
-  for (uint64_t w = blockIdx.x * blockDim.x + threadIdx.x; w < slots; w += stride) p.Q_prev[w] = kQEmpty;
+
 }
 
-template <int KT>
+template <int KT, typename PT>
 static void launch_k(const BloomParams& p, unsigned grid, int sm_count, cudaStream_t s) {
-  k3_probe<KT><<<grid, BL_THREADS, 0, s>>>(p);
-  k4_insert<KT><<<grid, BL_THREADS, 0, s>>>(p);
-  k5_resolve<KT><<<grid, BL_THREADS, 0, s>>>(p);
-  k6_verdict<KT><<<(unsigned)sm_count * 2, BL_THREADS, 0, s>>>(p);
+  k3_probe<KT, PT><<<grid, BL_THREADS, 0, s>>>(p);
+  k4_insert<KT, PT><<<grid, BL_THREADS, 0, s>>>(p);
+  k5_resolve<KT, PT><<<grid, BL_THREADS, 0, s>>>(p);
+  k6_verdict<KT, PT><<<(unsigned)sm_count * 2, BL_THREADS, 0, s>>>(p);
 }
 
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
   const uint64_t n = (uint64_t)p.nsb * p.bl;
   const unsigned grid = (unsigned)((n + BL_THREADS - 1) / BL_THREADS);
   cudaMemsetAsync(p.cand_count, 0, sizeof(uint32_t), s);
-  if (p.k == 17) launch_k<17>(p, grid, sm_count, s);   // every BASELINE config (p = 1e-5)
-  else launch_k<0>(p, grid, sm_count, s);
+  cudaMemsetAsync(p.Q, 0xFF, 8ull << p.q_log2, s);   // this sub-batch's E: all slots empty
+  if (p.k == 17) {                                      // every BASELINE config (p = 1e-5)
+    if (p.m <= (1ull << 32)) launch_k<17, uint32_t>(p, grid, sm_count, s);
+    else launch_k<17, uint64_t>(p, grid, sm_count, s);   // C5: m = 23,962,645,944
+  } else {
+    launch_k<0, uint64_t>(p, grid, sm_count, s);
+  }
   return 4;
 }
 

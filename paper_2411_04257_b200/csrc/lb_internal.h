@@ -40,7 +40,7 @@ struct MinhashParams {
 struct BloomParams {
   uint32_t* F;               // owned filters, bl * W uint32 words
   uint64_t* Q;               // compact earliest-setter table of this sub-batch (2^q_log2 slots)
-  uint64_t* Q_prev;          // the other buffer (previous sub-batch), reset to empty by K6
+  uint64_t* Q_prev;          // the other buffer (previous sub-batch)
   uint32_t q_log2;
   uint64_t W;                // uint32 words per band
   uint64_t m, m_inv;         // probe modulus and Barrett reciprocal
