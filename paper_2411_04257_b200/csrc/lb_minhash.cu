@@ -107,6 +107,7 @@ __device__ __forceinline__ uint32_t eval_fast(const PermCoef& c, const XLimbs& x
   return y;
 }
 
+
 __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
   uint64_t x = mod_p(fp);
   XLimbs l;
