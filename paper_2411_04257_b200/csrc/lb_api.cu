@@ -403,13 +403,14 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     p.tokens = b->tokens;
     p.tok_base = 0;
   } else {
-    if ((rc = validate_host(h, b->offsets, n))) return rc;
+    // No O(n) host pass: the offsets are validated on the device (K0), which gates every kernel;
+    // the host only checks what its own copies depend on (offsets[0], chunk bounds).
+    if (b->offsets[0] != 0) return fail(h, LSHBLOOM_EUSAGE, "offsets[0] must be 0");
     LB_CUDA(h, ensure(h->off, (n + 1) * sizeof(uint64_t)));
     LB_CUDA(h, cudaMemcpyAsync(h->off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    uint64_t maxdoc = 0;
-    for (uint64_t i = 0; i < n; i++) maxdoc = std::max(maxdoc, b->offsets[i + 1] - b->offsets[i]);
-    chunk_tokens = std::max(kChunkTokens, maxdoc);
-    const uint64_t buf_tokens = std::min(chunk_tokens, b->offsets[n]);
+    h->launches += launch_validate((const uint64_t*)h->off.p, n, h->d_err, s);
+    chunk_tokens = kChunkTokens;
+    const uint64_t buf_tokens = std::max<uint64_t>(1, std::min(chunk_tokens, b->offsets[n]));
     for (int i = 0; i < 2; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
     p.offsets = (const uint64_t*)h->off.p;
   }
@@ -431,7 +432,12 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       if (d1 <= d0) d1 = d0 + 1;
       d1 = std::min(d1, fuse_chunk_end(d0, n));
       const uint64_t t1 = b->offsets[d1];
+      if (t1 < t0) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease near index " + std::to_string(d0));
       const int buf = c & 1;
+      if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // one document larger than a chunk
+        LB_CUDA(h, cudaStreamSynchronize(s));
+        LB_CUDA(h, ensure(h->tok[buf], (t1 - t0) * sizeof(uint32_t)));
+      }
       LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
       LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, h->copy_stream));

@@ -442,6 +442,7 @@ static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int ma
   return 1;
 }
 
+
 template <int NPL, int UNR>
 static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
