@@ -250,6 +250,8 @@ def main():
 
     stream = torch.cuda.current_stream(dev)
 
+    step_wall = []   # host wall time per step (diagnostic only: every call synchronises its stream)
+
     def timed(fn, steps):
         barrier()
         torch.cuda.synchronize(dev)
@@ -257,25 +259,34 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         out = None
+        step_wall.clear()
         for _ in range(steps):
+            t0 = time.perf_counter()
             eng.reset()
             out = fn()
+            step_wall.append(1e3 * (time.perf_counter() - t0))
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
         return e0.elapsed_time(e1), out
 
+    def wall_summary():
+        w = sorted(step_wall)
+        return {"min": round(w[0], 3), "median": round(w[len(w) // 2], 3), "max": round(w[-1], 3)} if w else None
+
     # ---- device-resident arm
+    clk = ClockSampler(local)
+    clk.start()                                       # started before warm-up: its start-up is untimed
     for _ in range(args.warmup):
         eng.reset()
         flags = step(d_off, d_tok)
     torch.cuda.synchronize(dev)
     eng.stage_times(enable=True)                      # reset accumulators, start recording
     launches0 = eng.launch_count
-    clk = ClockSampler(local)
-    clk.start()
+    clk.lines.clear()
     ms, flags = timed(lambda: step(d_off, d_tok), args.steps)
     clocks = clk.stop()
+    device_step_wall = wall_summary()
     launches = eng.launch_count - launches0
     (k1_ms, bl_ms), (k1_n, bl_n) = eng.stage_times(enable=False)
     ms = max_over_ranks(ms)
@@ -298,7 +309,7 @@ def main():
         e2e_ms = max_over_ranks(e2e_ms)
         e2e = {"value": n_total * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(off.nbytes + tok.nbytes), "d2h_bytes_per_step": int(args.docs),
-               "ms_per_step": e2e_ms / args.steps}
+               "ms_per_step": e2e_ms / args.steps, "step_wall_ms": wall_summary()}
 
     if rank != 0:
         if world > 1:
@@ -349,6 +360,7 @@ def main():
                    "sub_batch": args.sub_batch or 32768, "csr_checksum_rank0": csum,
                    "dup_frac": dup_frac, "gen_s": round(gen_s, 1)},
         "roofline": roofline,
+        "step_wall_ms": device_step_wall,
         "stages_ms_per_step": {"minhash_k1": k1_ms / max(1, args.steps), "bloom_k3_k6": bl_ms / max(1, args.steps)},
         "cpu_baseline": cpu,
         "e2e": e2e,

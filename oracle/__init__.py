@@ -82,6 +82,16 @@ def _load():
         lib.orc_index_bits.argtypes = [vp, u32]
         lib.orc_index_query_insert.restype = i32
         lib.orc_index_query_insert.argtypes = [vp, u64, vp, u32, u32, i32, vp, vp]
+        lib.orc_classic_new.restype = vp
+        lib.orc_classic_new.argtypes = [u32]
+        lib.orc_classic_free.restype = None
+        lib.orc_classic_free.argtypes = [vp]
+        lib.orc_classic_keys.restype = u64
+        lib.orc_classic_keys.argtypes = [vp, u32]
+        lib.orc_classic_query_insert.restype = i32
+        lib.orc_classic_query_insert.argtypes = [vp, u64, vp, u32, u32, vp, vp]
+        lib.orc_optimal_params.restype = i32
+        lib.orc_optimal_params.argtypes = [dbl, u32, dbl, dbl, ctypes.POINTER(u32), ctypes.POINTER(u32)]
         _lib = lib
         return lib
 
@@ -234,3 +244,54 @@ def run(offsets, tokens, *, num_perm: int, b: int, r: int, n_expected: int, fp_r
     idx = index if index is not None else Index(b, n_expected, fp_rate, seed)
     dup = idx.query_insert(bh, nthreads=nthreads)
     return sig, bh, dup, idx
+
+
+class Classic:
+    """The classic MinHashLSH index (P:134 exact band equality): per band the set of
+    band hashes seen; a document is a duplicate iff some band hash of it was seen before."""
+
+    def __init__(self, b: int):
+        self._lib = _load()
+        self._h = self._lib.orc_classic_new(b)
+        if not self._h:
+            raise ValueError("orc_classic_new: b must be >= 1")
+        self.b = b
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._lib.orc_classic_free(h)
+
+    def keys(self, j: int) -> int:
+        """Distinct band-hash values stored for band j."""
+        return int(self._lib.orc_classic_keys(self._h, j))
+
+    def query_insert(self, bh, *, band_lo: int = 0, want_hits: bool = False):
+        arr = np.ascontiguousarray(bh, dtype=np.uint64)
+        n, ncol = arr.shape
+        dup = np.zeros(n, np.uint8)
+        hits = np.zeros((n, ncol), np.uint8) if want_hits else None
+        rc = self._lib.orc_classic_query_insert(self._h, n, _ptr(arr), band_lo, ncol, _ptr(dup),
+                                                _ptr(hits) if hits is not None else 0)
+        if rc:
+            raise OracleError(rc, "usage error")
+        return (dup, hits) if want_hits else dup
+
+
+def optimal_params(threshold: float, num_perm: int, fp_weight: float = 0.5,
+                   fn_weight: float = 0.5) -> tuple[int, int]:
+    """(b, r) minimising the weighted FP/FN areas of the LSH S-curve."""
+    b = ctypes.c_uint32()
+    r = ctypes.c_uint32()
+    if _load().orc_optimal_params(threshold, num_perm, fp_weight, fn_weight, ctypes.byref(b), ctypes.byref(r)):
+        raise ValueError("optimal_params: need 0 < threshold <= 1 and num_perm >= 2")
+    return int(b.value), int(r.value)
+
+
+def plan(n_docs: int, p_effective: float, threshold: float, num_perm: int) -> dict:
+    """Capacity plan (Tables 1-2): b from optimal_params, per-filter p from
+    p_effective = 1 - (1 - p)^b, m and k per filter, total = b * ceil(m / 8) bytes."""
+    b, r = optimal_params(threshold, num_perm)
+    p = -np.expm1(np.log1p(-p_effective) / b)
+    m, k = bloom_size(int(n_docs), float(p))
+    return {"b": b, "r": r, "p": float(p), "m": m, "k": k, "total_bytes": b * ((m + 7) // 8)}

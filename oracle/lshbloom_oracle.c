@@ -310,3 +310,126 @@ int orc_index_query_insert(void *p, uint64_t n_docs, const uint64_t *bh, uint32_
     free(hit); free(jobs); free(th);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* The classic MinHashLSH index ("if two bands ... are exactly      */
+/* identical ... candidate pairs"; S:186-189 ClassicLshIndex      */
+/* classic_insert / classic_query): b maps from band hash to the documents    */
+/* holding it.  A document is a classic duplicate iff some band hash of it    */
+/* was already inserted by an earlier document of the stream; then all its   */
+/* band hashes are inserted.  Only membership matters for that verdict, so    */
+/* each band keeps the set of band-hash values seen (a plain linear-probing   */
+/* hash set; band hashes are < P = 2^61 - 1, so UINT64_MAX marks empty).      */
+
+typedef struct {
+    uint64_t cap, used;
+    uint64_t *keys;
+} orc_set;
+
+static int orc_set_contains(const orc_set *S, uint64_t v) {
+    if (!S->cap) return 0;
+    uint64_t s = orc_mix64(v) & (S->cap - 1);
+    while (S->keys[s] != UINT64_MAX) {
+        if (S->keys[s] == v) return 1;
+        s = (s + 1) & (S->cap - 1);
+    }
+    return 0;
+}
+
+static void orc_set_add(orc_set *S, uint64_t v);
+
+static void orc_set_grow(orc_set *S) {
+    orc_set T = {S->cap ? 2 * S->cap : 1024, 0, NULL};
+    T.keys = malloc(8 * (size_t)T.cap);
+    memset(T.keys, 0xFF, 8 * (size_t)T.cap);
+    for (uint64_t i = 0; i < S->cap; i++)
+        if (S->keys[i] != UINT64_MAX) orc_set_add(&T, S->keys[i]);
+    free(S->keys);
+    *S = T;
+}
+
+static void orc_set_add(orc_set *S, uint64_t v) {
+    if (2 * (S->used + 1) > S->cap) orc_set_grow(S);
+    uint64_t s = orc_mix64(v) & (S->cap - 1);
+    while (S->keys[s] != UINT64_MAX) {
+        if (S->keys[s] == v) return;
+        s = (s + 1) & (S->cap - 1);
+    }
+    S->keys[s] = v;
+    S->used++;
+}
+
+typedef struct {
+    uint32_t b;
+    uint64_t doc_count;
+    orc_set *sets;
+} orc_classic;
+
+void *orc_classic_new(uint32_t b) {
+    if (b == 0) return NULL;
+    orc_classic *X = calloc(1, sizeof(orc_classic));
+    X->b = b;
+    X->sets = calloc(b, sizeof(orc_set));
+    return X;
+}
+
+void orc_classic_free(void *p) {
+    orc_classic *X = (orc_classic *)p;
+    if (!X) return;
+    for (uint32_t j = 0; j < X->b; j++) free(X->sets[j].keys);
+    free(X->sets); free(X);
+}
+
+uint64_t orc_classic_keys(void *p, uint32_t j) { return ((orc_classic *)p)->sets[j].used; }
+
+/* Stream order, one document at a time: query every band ("union over bands of ids in
+ * the bucket matching that band's hash"; non-empty = duplicate), then insert. */
+int orc_classic_query_insert(void *p, uint64_t n_docs, const uint64_t *bh, uint32_t band_lo,
+                             uint32_t ncol, uint8_t *dup_out, uint8_t *hits_out) {
+    orc_classic *X = (orc_classic *)p;
+    if (!X || band_lo + ncol > X->b) return 1;
+    for (uint64_t i = 0; i < n_docs; i++) {
+        uint8_t any = 0;
+        for (uint32_t c = 0; c < ncol; c++) {
+            uint8_t h = (uint8_t)orc_set_contains(&X->sets[band_lo + c], bh[i * ncol + c]);
+            any |= h;
+            if (hits_out) hits_out[i * ncol + c] = h;
+        }
+        for (uint32_t c = 0; c < ncol; c++) orc_set_add(&X->sets[band_lo + c], bh[i * ncol + c]);
+        if (dup_out) dup_out[i] = any;
+    }
+    X->doc_count += n_docs;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Band selection ("determine an optimal band size b", S:193-199   */
+/* optimal_params): over all b*r <= num_perm minimise                         */
+/*   fp_w * int_0^T (1-(1-s^r)^b) ds + fn_w * int_T^1 (1-s^r)^b ds           */
+/* with composite Simpson's rule, 1000 subintervals per integral;     */
+/* ties toward smaller b, then smaller r.                                     */
+
+static double orc_fp_integrand(double s, uint32_t b, uint32_t r) { return 1.0 - pow(1.0 - pow(s, r), b); }
+static double orc_fn_integrand(double s, uint32_t b, uint32_t r) { return pow(1.0 - pow(s, r), b); }
+
+static double orc_simpson(double (*f)(double, uint32_t, uint32_t), double lo, double hi, uint32_t b, uint32_t r) {
+    const int N = 1000;
+    double h = (hi - lo) / N, acc = f(lo, b, r) + f(hi, b, r);
+    for (int i = 1; i < N; i++) acc += f(lo + i * h, b, r) * ((i & 1) ? 4.0 : 2.0);
+    return acc * h / 3.0;
+}
+
+int orc_optimal_params(double T, uint32_t num_perm, double fp_w, double fn_w, uint32_t *b_out, uint32_t *r_out) {
+    if (!(T > 0.0 && T <= 1.0) || num_perm < 2) return 1;
+    double best = INFINITY;
+    uint32_t bb = 0, br = 0;
+    for (uint32_t b = 1; b <= num_perm; b++) {
+        for (uint32_t r = 1; b * r <= num_perm; r++) {
+            double e = fp_w * orc_simpson(orc_fp_integrand, 0.0, T, b, r) +
+                       fn_w * orc_simpson(orc_fn_integrand, T, 1.0, b, r);
+            if (e < best) { best = e; bb = b; br = r; }
+        }
+    }
+    *b_out = bb; *r_out = br;
+    return 0;
+}

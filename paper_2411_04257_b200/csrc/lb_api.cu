@@ -377,10 +377,19 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
 // sub-batches on bloom_stream as soon as its band hashes exist, so the integer-bound K1 of
 // chunk c+1 overlaps the memory-bound Bloom kernels of chunk c.  Bloom sub-batches stay in
 // document order (one stream), which is all the exact semantics need.
-constexpr uint64_t kFuseDocs = 131072;
 constexpr uint64_t kFuseEdgeDocs = 32768;   // small first / last chunks: Bloom starts early, short tail
 
+uint64_t fuse_docs() {
+  static uint64_t v = 0;
+  if (!v) {
+    const char* e = getenv("LSHBLOOM_FUSE_DOCS");
+    v = e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 131072;
+  }
+  return v;
+}
+
 uint64_t fuse_chunk_end(uint64_t d0, uint64_t n) {
+  const uint64_t kFuseDocs = fuse_docs();
   if (d0 == 0) return std::min(n, kFuseEdgeDocs);
   const uint64_t left = n - d0;
   if (left <= kFuseEdgeDocs) return n;
