@@ -96,7 +96,22 @@ typedef struct {
     uint32_t world;      /*   over world ranks (bands split as evenly as possible) */
     uint32_t sub_batch;  /* documents per Bloom sub-batch (0 = default 32768); results do
                             not depend on it */
+    uint32_t index_kind; /* LSHBLOOM_INDEX_BLOOM (0, the paper's method) or
+                            LSHBLOOM_INDEX_CLASSIC (1, see below) */
 } lshbloom_config;
+
+/* Index kinds.
+ * LSHBLOOM_INDEX_BLOOM: one Bloom filter per band -- the paper's method.
+ * LSHBLOOM_INDEX_CLASSIC: the classic MinHashLSH index it replaces (P:134 exact band
+ *   equality): per band the set of band hashes seen, a document being a
+ *   duplicate iff one of its band hashes was inserted by an earlier document.  Same entry
+ *   points and stream semantics; no false positives beyond LSH's own (the Bloom
+ *   index's duplicates contain these).  Device memory: per owned band 16 B x cap slots,
+ *   cap = the power of two >= n_expected / 0.7; a batch that would take doc_count past
+ *   0.9 cap is rejected (error 1) before any mutation.  fp_rate is ignored; filter_copy and
+ *   save/load return error 1. */
+#define LSHBLOOM_INDEX_BLOOM 0
+#define LSHBLOOM_INDEX_CLASSIC 1
 
 typedef struct {
     uint64_t m;               /* bits per filter (analytic, the probe modulus) */
@@ -111,6 +126,8 @@ typedef struct {
     uint64_t seed;
     uint64_t n_expected;
     double fp_rate;
+    uint32_t index_kind;      /* LSHBLOOM_INDEX_BLOOM / _CLASSIC */
+    uint64_t classic_slots;   /* classic: table slots per band (0 for Bloom) */
 } lshbloom_info_t;
 
 /* Create an index of b Bloom filters: sizes them from (n_expected, fp_rate),

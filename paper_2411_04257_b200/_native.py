@@ -35,7 +35,7 @@ class _Config(ctypes.Structure):
                 ("shingle_n", ctypes.c_uint32), ("n_expected", ctypes.c_uint64),
                 ("fp_rate", ctypes.c_double), ("seed", ctypes.c_uint64),
                 ("device", ctypes.c_int32), ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32),
-                ("sub_batch", ctypes.c_uint32)]
+                ("sub_batch", ctypes.c_uint32), ("index_kind", ctypes.c_uint32)]
 
 
 class _Info(ctypes.Structure):
@@ -45,7 +45,8 @@ class _Info(ctypes.Structure):
                 ("words_per_band", ctypes.c_uint64), ("filter_bytes", ctypes.c_uint64),
                 ("p_eff", ctypes.c_double), ("doc_count", ctypes.c_uint64),
                 ("oversubscribed", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("n_expected", ctypes.c_uint64), ("fp_rate", ctypes.c_double)]
+                ("n_expected", ctypes.c_uint64), ("fp_rate", ctypes.c_double),
+                ("index_kind", ctypes.c_uint32), ("classic_slots", ctypes.c_uint64)]
 
 
 EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloom_signatures",
@@ -119,8 +120,13 @@ class LSHBloom:
 
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, shingle_n: int = 5, device: int | None = None, rank: int = 0, world: int = 1,
-                 sub_batch: int = 0, _handle=None):
+                 sub_batch: int = 0, index: str = "bloom", _handle=None):
+        """index: "bloom" (the paper's per-band Bloom filters) or "classic" (the exact
+        band-equality MinHashLSH index it replaces; fp_rate is ignored)."""
         self._lib = lib()
+        kinds = {"bloom": 0, "classic": 1}
+        if index not in kinds:
+            raise ValueError("index must be 'bloom' or 'classic'")
         if device is None:
             try:
                 import torch
@@ -129,7 +135,7 @@ class LSHBloom:
                 device = -1
         if _handle is None:
             cfg = _Config(num_perm, b, r, shingle_n, n_expected, fp_rate, seed & (2**64 - 1), device,
-                          rank, world, sub_batch)
+                          rank, world, sub_batch, kinds[index])
             h = ctypes.c_void_p()
             rc = self._lib.lshbloom_create_ex(ctypes.byref(cfg), ctypes.byref(h))
             if rc:
@@ -141,6 +147,7 @@ class LSHBloom:
         self.device = device
         self.m, self.k = inf["m"], inf["k"]
         self.band_lo, self.band_hi = inf["band_lo"], inf["band_hi"]
+        self.index = "classic" if inf["index_kind"] == 1 else "bloom"
 
     # ------------------------------------------------------------------ plumbing
     def close(self):

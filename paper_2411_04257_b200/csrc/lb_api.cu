@@ -68,6 +68,10 @@ struct lshbloom {
   ErrState* d_err = nullptr;
   DevBuf off, tok[2], bh, dup, sig;
   uint64_t doc_count = 0, launches = 0;
+  // classic MinHashLSH index (index_kind = LSHBLOOM_INDEX_CLASSIC)
+  uint64_t* d_ckeys = nullptr;    // [bl][2^c_log2cap]
+  uint64_t* d_cvals = nullptr;
+  uint32_t c_log2cap = 0;
   // stage timing (lshbloom_stage_times)
   bool timing = false;
   cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -124,7 +128,7 @@ int check_handle(lshbloom* h) {
 void free_all(lshbloom* h) {
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_ekey);
-  F(h->d_eval); F(h->d_st); F(h->d_cand); F(h->d_counters); F(h->d_err);
+  F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p);
   for (int i = 0; i < 2; i++) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
@@ -325,9 +329,47 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
   return LSHBLOOM_OK;
 }
 
+// Classic index (lb_classic.cu): KC1 + KC2 over batch documents [i_begin, i_end).
+int run_classic(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin,
+                uint64_t i_end, uint8_t* dup_dev, cudaStream_t s, bool first, bool last) {
+  ClassicParams p;
+  memset(&p, 0, sizeof p);
+  p.keys = h->d_ckeys;
+  p.vals = h->d_cvals;
+  p.log2cap = h->c_log2cap;
+  p.bl = h->bl;
+  p.doc_base = h->doc_count;
+  p.bh = bh_dev;
+  p.bh_sj = bh_sj;
+  p.bh_si = bh_si;
+  p.i0 = (uint32_t)i_begin;
+  p.n = (uint32_t)(i_end - i_begin);
+  p.dup = dup_dev;
+  p.full = (int*)h->d_counters + 8;
+  p.err = &h->d_err->pad;
+  if (first) stage_begin(h, 1, s);
+  if (p.n) h->launches += launch_classic(p, s);
+  LB_CUDA(h, cudaGetLastError());
+  if (last) stage_end(h, 1, s);
+  return LSHBLOOM_OK;
+}
+
+// Classic index capacity: the batch may not take doc_count past 0.9 of the table (checked
+// before any mutation, so the probe loops always find a free slot).
+int classic_capacity(lshbloom* h, uint64_t n) {
+  if (h->cfg.index_kind != LSHBLOOM_INDEX_CLASSIC) return LSHBLOOM_OK;
+  const double cap = (double)(1ull << h->c_log2cap);
+  if ((double)(h->doc_count + n) > 0.9 * cap)
+    return fail(h, LSHBLOOM_EUSAGE, "classic index full: doc_count + batch > 0.9 x " + std::to_string((uint64_t)cap) +
+                                        " slots (raise n_expected)");
+  return LSHBLOOM_OK;
+}
+
 // K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
 int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin, uint64_t i_end,
               uint8_t* dup_dev, cudaStream_t s, bool first = true, bool last = true) {
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC)
+    return run_classic(h, bh_dev, bh_sj, bh_si, i_begin, i_end, dup_dev, s, first, last);
   BloomParams p;
   memset(&p, 0, sizeof p);
   p.F = h->d_F;
@@ -501,6 +543,7 @@ int lshbloom_create(uint32_t num_perm, uint32_t b, uint32_t r, uint64_t n_expect
   c.rank = 0;
   c.world = 1;
   c.sub_batch = 0;
+  c.index_kind = LSHBLOOM_INDEX_BLOOM;
   return lshbloom_create_ex(&c, out);
 }
 
@@ -514,13 +557,17 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   if (c.r == 0 || (uint64_t)c.b * c.r > c.num_perm) return fail(nullptr, LSHBLOOM_EUSAGE, "need r >= 1 and b*r <= num_perm (S:183)");
   if (c.shingle_n == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "shingle_n must be >= 1");
   if (c.n_expected == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "n_expected must be >= 1");
-  if (!(c.fp_rate > 0.0 && c.fp_rate < 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "fp_rate must be in (0, 1) (S:273)");
+  if (c.index_kind > LSHBLOOM_INDEX_CLASSIC) return fail(nullptr, LSHBLOOM_EUSAGE, "index_kind must be 0 (Bloom) or 1 (classic)");
+  const bool classic = c.index_kind == LSHBLOOM_INDEX_CLASSIC;
+  if (!classic && !(c.fp_rate > 0.0 && c.fp_rate < 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "fp_rate must be in (0, 1) (S:273)");
   if (c.world == 0) c.world = 1;
   if (c.rank >= c.world) return fail(nullptr, LSHBLOOM_EUSAGE, "rank must be < world");
   if (c.world > c.b) return fail(nullptr, LSHBLOOM_EUSAGE, "world must be <= b (every rank owns >= 1 band)");
 
   // Sizing, P:224-225 / S:263 (DESIGN R9): natural log, ceil for m, llround for k.
-  const double md = ceil(-(double)c.n_expected * log(c.fp_rate) / (log(2.0) * log(2.0)));
+  // (The classic index has no filters; a nominal p keeps the arithmetic below finite.)
+  const double psz = classic ? 0.5 : c.fp_rate;
+  const double md = ceil(-(double)c.n_expected * log(psz) / (log(2.0) * log(2.0)));
   if (!(md >= 1.0) || md >= 68719476736.0) return fail(nullptr, LSHBLOOM_EUSAGE, "filter size m must be < 2^36 bits");
   long long kk = llround((md / (double)c.n_expected) * log(2.0));
   if (kk < 1) kk = 1;
@@ -608,6 +655,29 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaMalloc(&h->d_s2, h->bl * 8));
   CR(cudaMemcpy(h->d_s1, s1.data(), h->bl * 8, cudaMemcpyHostToDevice));
   CR(cudaMemcpy(h->d_s2, s2.data(), h->bl * 8, cudaMemcpyHostToDevice));
+
+  if (classic) {
+    // per owned band 2^c_log2cap slots, load factor <= 0.7 at n_expected documents
+    uint32_t lg = 10;
+    while ((double)(1ull << lg) * 0.7 < (double)c.n_expected) lg++;
+    if (lg > 40) { free_all(h); delete h; return fail(nullptr, LSHBLOOM_EUSAGE, "n_expected too large for the classic index"); }
+    h->c_log2cap = lg;
+    h->m = 0;
+    h->k = 0;
+    h->W = 0;
+    const size_t tbytes = ((size_t)h->bl << lg) * 8;
+    CR(cudaMalloc(&h->d_ckeys, tbytes));
+    CR(cudaMalloc(&h->d_cvals, tbytes));
+    CR(cudaMemset(h->d_ckeys, 0xFF, tbytes));   // all slots empty
+    CR(cudaMemset(h->d_cvals, 0xFF, tbytes));   // no document yet
+    CR(cudaMalloc(&h->d_counters, 16 * 4));
+    CR(cudaMemset(h->d_counters, 0, 16 * 4));
+    CR(cudaMalloc(&h->d_err, sizeof(ErrState)));
+    CR(cudaMemset(h->d_err, 0, sizeof(ErrState)));
+    CR(cudaDeviceSynchronize());
+    *out = h;
+    return LSHBLOOM_OK;
+  }
 
   // Filters "with all bits initially set to 0".
   const size_t fbytes = (size_t)h->bl * h->W * 4;
@@ -712,6 +782,7 @@ int lshbloom_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out
   if (rc) return rc;
   if ((rc = check_batch(h, b))) return rc;
   if (!dup_out) return fail(h, LSHBLOOM_EUSAGE, "NULL dup_out");
+  if ((rc = classic_capacity(h, b->n_docs))) return rc;
   DeviceGuard g(h->device);
   cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
   const uint64_t n = b->n_docs;
@@ -734,6 +805,7 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   if (rc) return rc;
   if (!bh_owned || !hit_out) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_owned / hit_out");
   if (n_docs == 0 || n_docs > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_docs must be in [1, 2^32)");
+  if ((rc = classic_capacity(h, n_docs))) return rc;
   DeviceGuard g(h->device);
   cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
   const size_t bytes = n_docs * h->bl * sizeof(uint64_t);
@@ -759,7 +831,13 @@ int lshbloom_reset(lshbloom* h) {
   int rc = check_handle(h);
   if (rc) return rc;
   DeviceGuard g(h->device);
-  LB_CUDA(h, cudaMemsetAsync(h->d_F, 0, (size_t)h->bl * h->W * 4, h->own_stream));
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) {
+    const size_t tbytes = ((size_t)h->bl << h->c_log2cap) * 8;
+    LB_CUDA(h, cudaMemsetAsync(h->d_ckeys, 0xFF, tbytes, h->own_stream));
+    LB_CUDA(h, cudaMemsetAsync(h->d_cvals, 0xFF, tbytes, h->own_stream));
+  } else {
+    LB_CUDA(h, cudaMemsetAsync(h->d_F, 0, (size_t)h->bl * h->W * 4, h->own_stream));
+  }
   LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
   h->doc_count = 0;
   return LSHBLOOM_OK;
@@ -769,6 +847,7 @@ int lshbloom_filter_copy(lshbloom* h, uint32_t j, uint32_t* dst) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (!dst || j < h->band_lo || j >= h->band_hi) return fail(h, LSHBLOOM_EUSAGE, "band not owned by this handle / NULL dst");
+  if (h->cfg.index_kind != LSHBLOOM_INDEX_BLOOM) return fail(h, LSHBLOOM_EUSAGE, "not a Bloom index");
   DeviceGuard g(h->device);
   LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
   LB_CUDA(h, cudaMemcpy(dst, h->d_F + (uint64_t)(j - h->band_lo) * h->W, h->W * 4, cudaMemcpyDeviceToHost));
@@ -794,6 +873,13 @@ int lshbloom_info(const lshbloom* h, lshbloom_info_t* out) {
   out->seed = h->cfg.seed;
   out->n_expected = h->cfg.n_expected;
   out->fp_rate = h->cfg.fp_rate;
+  out->index_kind = h->cfg.index_kind;
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) {
+    out->classic_slots = 1ull << h->c_log2cap;
+    out->filter_bytes = ((uint64_t)h->bl << h->c_log2cap) * 16;
+    out->p_eff = 0.0;
+    out->oversubscribed = (double)h->doc_count > 0.7 * (double)out->classic_slots ? 1 : 0;
+  }
   return LSHBLOOM_OK;
 }
 
@@ -901,6 +987,7 @@ int lshbloom_save(lshbloom* h, const char* path) {
   if (rc) return rc;
   if (!path) return fail(h, LSHBLOOM_EUSAGE, "NULL path");
   if (h->cfg.world != 1) return fail(h, LSHBLOOM_EUSAGE, "save needs an unsharded handle (world = 1)");
+  if (h->cfg.index_kind != LSHBLOOM_INDEX_BLOOM) return fail(h, LSHBLOOM_EUSAGE, "save: not a Bloom index");
   if (h->cfg.shingle_n != 5) return fail(h, LSHBLOOM_EUSAGE, "the LSHB format carries no shingle width; save needs n = 5");
   DeviceGuard g(h->device);
   LB_CUDA(h, cudaDeviceSynchronize());

@@ -62,6 +62,19 @@ struct BloomParams {
   const int* err;
 };
 
+struct ClassicParams {        // classic MinHashLSH index (lb_classic.cu)
+  uint64_t* keys;            // [bl][2^log2cap] band hashes (~0 = empty slot)
+  uint64_t* vals;            // [bl][2^log2cap] earliest global document index per key
+  uint32_t log2cap, bl;
+  uint64_t doc_base;         // global index of batch document 0
+  const uint64_t* bh;        // band hashes: owned band jl of doc i at bh[jl*bh_sj + i*bh_si]
+  uint64_t bh_sj, bh_si;
+  uint32_t i0, n;            // batch documents [i0, i0 + n)
+  uint8_t* dup;              // [batch] flags (OR over owned bands)
+  int* full;                 // set if a probe sequence wrapped (cannot happen at load <= 0.9)
+  const int* err;
+};
+
 struct ErrState {
   int flags;                 // bit0: usage (offsets[0] != 0 or decreasing)
   int pad;
@@ -72,5 +85,6 @@ struct ErrState {
 int launch_validate(const uint64_t* offsets, uint64_t n_docs, ErrState* err, cudaStream_t s);
 int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps);
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s);
+int launch_classic(const ClassicParams& p, cudaStream_t s);
 
 }  // namespace lb

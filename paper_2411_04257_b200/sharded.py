@@ -29,7 +29,8 @@ def band_range(rank: int, world: int, b: int) -> tuple[int, int]:
 
 class ShardedLSHBloom:
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
-                 *, group=None, device: int | None = None, sub_batch: int = 0, engine=None):
+                 *, group=None, device: int | None = None, sub_batch: int = 0, index: str = "bloom",
+                 engine=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -37,7 +38,7 @@ class ShardedLSHBloom:
         if engine is None:
             from ._native import LSHBloom
             engine = LSHBloom(num_perm, b, r, n_expected, fp_rate, seed, device=device,
-                              rank=self.rank, world=self.world, sub_batch=sub_batch)
+                              rank=self.rank, world=self.world, sub_batch=sub_batch, index=index)
         self.engine = engine
         self.band_lo, self.band_hi = band_range(self.rank, self.world, b)
         assert (engine.band_lo, engine.band_hi) == (self.band_lo, self.band_hi)

@@ -2,7 +2,7 @@
 // loads and atomicOr read-modify-writes over a buffer much larger than L2, i.e. the denominator
 // the Bloom stage's HBM roofline is compared against.  Each access touches one 32-B sector.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o rand_sector rand_sector.cu
-//   ./rand_sector [GB=48]
+//   ./rand_sector [GB=48] [l2_fetch_granularity_bytes]
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -39,13 +39,27 @@ __global__ void k(uint32_t* buf, uint64_t words, uint64_t n_threads, uint64_t sa
   } else if (MODE == 2) {
 #pragma unroll
     for (int i = 0; i < 17; i++) atomicOr(buf + pos[i], 1u << (i & 31));
-  } else {
+  } else if (MODE == 3) {
     uint32_t v[17];
 #pragma unroll
     for (int i = 0; i < 17; i++) v[i] = __ldcg(buf + pos[i]);
 #pragma unroll
     for (int i = 0; i < 17; i++)
       if (!(v[i] & 1u)) acc |= atomicOr(buf + pos[i], 1u);
+  } else if (MODE == 4) {   // L2 prefetch of every line, then the atomics without waiting
+#pragma unroll
+    for (int i = 0; i < 17; i++) asm volatile("prefetch.global.L2 [%0];" ::"l"(buf + pos[i]));
+    uint32_t v[17];
+#pragma unroll
+    for (int i = 0; i < 17; i++) v[i] = atomicOr(buf + pos[i], 1u << (i & 31));
+#pragma unroll
+    for (int i = 0; i < 17; i++) acc |= v[i];
+  } else {                  // MODE 5: loads, then atomics on every word (like K4 after a reload)
+    uint32_t v[17];
+#pragma unroll
+    for (int i = 0; i < 17; i++) v[i] = __ldcg(buf + pos[i]);
+#pragma unroll
+    for (int i = 0; i < 17; i++) acc |= atomicOr(buf + pos[i], v[i] | 2u);
   }
   if (acc == 0x12345678u) sink[0] = acc;
 }
@@ -74,6 +88,16 @@ void run(const char* name, uint32_t* buf, uint64_t words, uint32_t* sink) {
 
 int main(int argc, char** argv) {
   const double gb = argc > 1 ? atof(argv[1]) : 48.0;
+  if (argc > 2) {   // cudaLimitMaxL2FetchGranularity (bytes): how much L2 fetches from DRAM per miss
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[2]));
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("{\"l2_fetch_granularity\": %zu, \"set\": \"%s\"}\n", v, cudaGetErrorString(e));
+  } else {
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("{\"l2_fetch_granularity_default\": %zu}\n", v);
+  }
   const uint64_t words = (uint64_t)(gb * 1e9 / 4);
   uint32_t *buf, *sink;
   if (cudaMalloc(&buf, words * 4) != cudaSuccess) { printf("alloc failed\n"); return 1; }
@@ -85,5 +109,7 @@ int main(int argc, char** argv) {
   run<1>("atomicOr_ret", buf, words, sink);
   cudaMemset(buf, 0, words * 4);
   run<3>("load_then_atomicOr", buf, words, sink);
+  run<4>("prefetchL2_then_atomicOr", buf, words, sink);
+  run<5>("load_then_atomicOr_all", buf, words, sink);
   return 0;
 }
