@@ -206,6 +206,30 @@ LSHBLOOM_API int lshbloom_stage_times(lshbloom *h, int32_t enable, double *ms_ou
 LSHBLOOM_API int lshbloom_save(lshbloom *h, const char *path);
 LSHBLOOM_API int lshbloom_load(const char *path, int32_t device, lshbloom **out);
 
+/* Band selection and capacity planning (host-only).
+ * lshbloom_optimal_params: the (b, r) with b*r <= num_perm minimising
+ *   fp_weight * int_0^T (1 - (1 - s^r)^b) ds + fn_weight * int_T^1 (1 - s^r)^b ds
+ * ("given a desired Jaccard similarity threshold, T, one can determine an optimal band
+ * size, b"), each integral by composite Simpson's rule with 1000 subintervals
+ * (S:232); ties go to the smaller b, then the smaller r.  T in (0, 1], num_perm >= 2,
+ * weights >= 0; error 1 otherwise.  (T = 0.8, 128 permutations -> b = 9.)
+ * lshbloom_plan: sizes an index for n_docs documents at an effective false-positive rate
+ * p_effective (P:227 p_eff = 1 - (1 - p)^b, inverted for the per-filter p) with b from
+ * lshbloom_optimal_params(T, num_perm, 0.5, 0.5) and m, k per filter as lshbloom_create does;
+ * total_bytes = b * ceil(m / 8) (Tables 1-2; P:229's 590 GB). */
+typedef struct {
+    uint32_t b, r;
+    double p;                 /* per-filter false-positive rate */
+    uint64_t m;               /* bits per filter */
+    uint32_t k;               /* probes per band hash */
+    uint64_t total_bytes;     /* b * ceil(m / 8) */
+} lshbloom_plan_t;
+
+LSHBLOOM_API int lshbloom_optimal_params(double threshold, uint32_t num_perm, double fp_weight,
+                                         double fn_weight, uint32_t *b_out, uint32_t *r_out);
+LSHBLOOM_API int lshbloom_plan(uint64_t n_docs, double p_effective, double threshold, uint32_t num_perm,
+                               lshbloom_plan_t *out);
+
 /* Number of kernel launches the library issued since create (launch-count evidence). */
 LSHBLOOM_API uint64_t lshbloom_launch_count(const lshbloom *h);
 

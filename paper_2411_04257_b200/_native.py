@@ -49,11 +49,16 @@ class _Info(ctypes.Structure):
                 ("index_kind", ctypes.c_uint32), ("classic_slots", ctypes.c_uint64)]
 
 
+class _Plan(ctypes.Structure):
+    _fields_ = [("b", ctypes.c_uint32), ("r", ctypes.c_uint32), ("p", ctypes.c_double),
+                ("m", ctypes.c_uint64), ("k", ctypes.c_uint32), ("total_bytes", ctypes.c_uint64)]
+
+
 EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloom_signatures",
            "lshbloom_band_hashes", "lshbloom_band_hashes_sharded", "lshbloom_query_insert",
            "lshbloom_query_insert_bands", "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info",
            "lshbloom_stage_times", "lshbloom_save", "lshbloom_load", "lshbloom_last_error",
-           "lshbloom_launch_count")
+           "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan")
 
 
 def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
@@ -79,9 +84,12 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     lib.lshbloom_last_error.argtypes = [vp]
     lib.lshbloom_last_error.restype = ctypes.c_char_p
     lib.lshbloom_launch_count.argtypes = [vp]
+    lib.lshbloom_optimal_params.argtypes = [ctypes.c_double, u32, ctypes.c_double, ctypes.c_double,
+                                            ctypes.POINTER(u32), ctypes.POINTER(u32)]
+    lib.lshbloom_plan.argtypes = [u64, ctypes.c_double, ctypes.c_double, u32, ctypes.POINTER(_Plan)]
     lib.lshbloom_launch_count.restype = u64
     for f in EXPORTS:
-        if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count"):
+        if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan"):
             getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -274,3 +282,23 @@ class LSHBloom:
 def _torch_dtype(name: str):
     import torch
     return getattr(torch, name)
+
+
+def optimal_params(threshold: float, num_perm: int, fp_weight: float = 0.5, fn_weight: float = 0.5):
+    """(b, r) minimising the weighted S-curve error areas (lshbloom_optimal_params; host-only)."""
+    b, r = ctypes.c_uint32(), ctypes.c_uint32()
+    L = lib()
+    rc = L.lshbloom_optimal_params(threshold, num_perm, fp_weight, fn_weight, ctypes.byref(b), ctypes.byref(r))
+    if rc:
+        raise LSHBloomError(rc, L.lshbloom_last_error(None).decode())
+    return int(b.value), int(r.value)
+
+
+def plan(n_docs: int, p_effective: float, threshold: float = 0.8, num_perm: int = 128) -> dict:
+    """Capacity plan of an index (lshbloom_plan; host-only): b, r, per-filter p, m, k, total bytes."""
+    out = _Plan()
+    L = lib()
+    rc = L.lshbloom_plan(int(n_docs), p_effective, threshold, num_perm, ctypes.byref(out))
+    if rc:
+        raise LSHBloomError(rc, L.lshbloom_last_error(None).decode())
+    return {f: getattr(out, f) for f, _ in _Plan._fields_}

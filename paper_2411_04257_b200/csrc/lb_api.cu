@@ -887,6 +887,59 @@ const char* lshbloom_last_error(const lshbloom* h) { return h ? h->err.c_str() :
 
 uint64_t lshbloom_launch_count(const lshbloom* h) { return h ? h->launches : 0; }
 
+// S-curve objective of a (b, r) pair: weighted areas of false positives
+// below T and false negatives above T, composite Simpson with 1000 subintervals.
+static double scurve_area(double lo, double hi, uint32_t b, uint32_t r, bool fn) {
+  const int N = 1000;
+  const double h = (hi - lo) / N;
+  auto f = [&](double s) {
+    const double miss = std::pow(1.0 - std::pow(s, (double)r), (double)b);   // P(no band collides)
+    return fn ? miss : 1.0 - miss;
+  };
+  double acc = f(lo) + f(hi);
+  for (int i = 1; i < N; i++) acc += (i % 2 ? 4.0 : 2.0) * f(lo + i * h);
+  return acc * h / 3.0;
+}
+
+int lshbloom_optimal_params(double threshold, uint32_t num_perm, double fp_weight, double fn_weight,
+                            uint32_t* b_out, uint32_t* r_out) {
+  if (!b_out || !r_out) return fail(nullptr, LSHBLOOM_EUSAGE, "NULL output");
+  if (!(threshold > 0.0 && threshold <= 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "threshold must be in (0, 1]");
+  if (num_perm < 2) return fail(nullptr, LSHBLOOM_EUSAGE, "num_perm must be >= 2");
+  if (!(fp_weight >= 0.0 && fn_weight >= 0.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "weights must be >= 0");
+  double best = INFINITY;
+  uint32_t bb = 0, br = 0;
+  for (uint32_t b = 1; b <= num_perm; b++)
+    for (uint32_t r = 1; (uint64_t)b * r <= num_perm; r++) {
+      const double e = fp_weight * scurve_area(0.0, threshold, b, r, false) +
+                       fn_weight * scurve_area(threshold, 1.0, b, r, true);
+      if (e < best) {   // strict: ties keep the smaller b, then the smaller r
+        best = e;
+        bb = b;
+        br = r;
+      }
+    }
+  *b_out = bb;
+  *r_out = br;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_plan(uint64_t n_docs, double p_effective, double threshold, uint32_t num_perm, lshbloom_plan_t* out) {
+  if (!out) return fail(nullptr, LSHBLOOM_EUSAGE, "NULL output");
+  if (n_docs == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "n_docs must be >= 1");
+  if (!(p_effective > 0.0 && p_effective < 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "p_effective must be in (0, 1)");
+  memset(out, 0, sizeof *out);
+  int rc = lshbloom_optimal_params(threshold, num_perm, 0.5, 0.5, &out->b, &out->r);
+  if (rc) return rc;
+  out->p = -std::expm1(std::log1p(-p_effective) / out->b);    // 1-(1-p)^b = p_eff
+  const double md = std::ceil(-(double)n_docs * std::log(out->p) / (std::log(2.0) * std::log(2.0)));
+  long long kk = std::llround((md / (double)n_docs) * std::log(2.0));
+  out->m = (uint64_t)md;
+  out->k = (uint32_t)(kk < 1 ? 1 : kk);
+  out->total_bytes = (uint64_t)out->b * ((out->m + 7) / 8);
+  return LSHBLOOM_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------------------------

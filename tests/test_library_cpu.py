@@ -108,3 +108,35 @@ def test_product_path_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "lshbloom_oracle" not in text, f
+
+
+# --------------------------------------------------------------------------- host planner
+# lshbloom_optimal_params / lshbloom_plan are host-only (no CUDA); compared with the oracle's
+# independently written planner (pinned in tests/test_oracle_classic.py) and the paper.
+
+@pytest.mark.parametrize("T,num_perm", [(0.8, 128), (0.5, 48), (0.3, 64), (0.9, 32), (0.7, 256), (1.0, 16)])
+def test_library_optimal_params_matches_oracle(lib, T, num_perm):
+    import oracle
+    assert pkg.optimal_params(T, num_perm) == oracle.optimal_params(T, num_perm)
+
+
+def test_library_plan_matches_oracle_and_paper(lib):
+    import oracle
+    for n, pe, T, npm in [(5e9, 1e-5, 0.8, 128), (1e10, 1e-10, 0.8, 128), (1e11, 1e-5, 0.8, 128),
+                          (39e6, 1e-4, 0.5, 256)]:
+        got, want = pkg.plan(int(n), pe, T, npm), oracle.plan(int(n), pe, T, npm)
+        for key in ("b", "r", "m", "k", "total_bytes"):
+            assert got[key] == want[key], (n, key)
+    assert round(pkg.plan(int(5e9), 1e-5)["total_bytes"] / 1e9, 2) == 160.51     # Table 1
+
+
+def test_library_planner_rejects_bad_arguments(lib):
+    for T in (0.0, 1.5, float("nan")):
+        with pytest.raises(LSHBloomError):
+            pkg.optimal_params(T, 128)
+    with pytest.raises(LSHBloomError):
+        pkg.optimal_params(0.8, 1)
+    with pytest.raises(LSHBloomError):
+        pkg.plan(0, 1e-5)
+    with pytest.raises(LSHBloomError):
+        pkg.plan(100, 1.0)
