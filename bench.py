@@ -16,6 +16,7 @@ with pinned HOST buffers (H2D of the CSR batch and D2H of the flags inside the t
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -47,6 +48,8 @@ def parse():
     ap.add_argument("--sub-batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hbm", action="store_true", help="skip the HBM-resident Bloom leg (C5 geometry)")
+    ap.add_argument("--hbm-docs", type=int, default=1_000_000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
     return ap.parse_args()
 
@@ -73,8 +76,11 @@ class ClockSampler:
 
     def start(self):
         try:
+            if os.environ.get("LSHBLOOM_BENCH_NO_CLOCKS"):   # diagnostic: measure the sampler's own cost
+                raise RuntimeError("disabled")
+            ms = os.environ.get("LSHBLOOM_BENCH_CLOCK_MS", "200")
             self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                          "-lms", ms, "-i", str(self.gpu)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -197,6 +203,60 @@ def run_reference(args, cfg):
     return 0
 
 
+# --------------------------------------------------------------------------- HBM-resident Bloom leg
+
+def hbm_leg(args, torch, dev, peaks, peak_src):
+    """The Bloom stage where it is HBM-bound: C5's index geometry (128 perms, b=20 r=6,
+    n_expected=1e9 -> 20 x 3.0 GB filters, m > 2^32) over C5's first documents, one fused
+    lshbloom_query_insert per step on freshly zeroed filters (every probe sets a new bit: the
+    stage's worst case).  Timed with CUDA events around the call; the library's stage events
+    give the Bloom (K3-K6) time.  Algorithmic traffic per probe = one 32-B sector read + one
+    32-B sector write-back; B200 moves a whole 128-B line per random access, which
+    the measured random-access peak (tools/micro/rand_sector.cu) reflects."""
+    from paper_2411_04257_b200 import LSHBloom
+    cfg = CONFIGS["C5"]
+    n = args.hbm_docs
+    off, tok = gen_range(cfg, 0, n)
+    d_off = torch.from_numpy(off.view(np.int64)).to(dev)
+    d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
+    eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=dev.index)
+    stream = torch.cuda.current_stream(dev)
+    steps, warm = max(3, min(args.steps, 10)), 2
+    tot = 0.0
+    for i in range(warm + steps):
+        eng.reset()
+        if i == warm:
+            eng.stage_times(enable=True)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        flags = eng.query_insert(d_off, d_tok)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= warm:
+            tot += e0.elapsed_time(e1)
+    (k1_ms, bl_ms), (k1_n, bl_n) = eng.stage_times(enable=False)
+    info = eng.info()
+    probes = n * cfg.b * eng.k
+    bl_step = bl_ms / max(1, bl_n)
+    alg_bytes = probes * 64.0
+    peak = float(peaks.get("hbm_gbs", 6546.0))
+    res = {"bound": "hbm", "workload": "C5 geometry (128 perms, b=20 r=6, n_expected=1e9, %.1f GB filters), "
+                                      "first %d C5 documents per step, fresh filters" % (info["filter_bytes"] / 1e9, n),
+           "docs_per_s": n * steps / (tot / 1e3), "ms_per_step": tot / steps,
+           "bloom_ms_per_step": bl_step, "probes_per_step": probes,
+           "Gprobe_per_s": probes / bl_step / 1e6,
+           "achieved": alg_bytes / bl_step / 1e6, "peak": peak, "unit": "GB/s", "frac": alg_bytes / bl_step / 1e6 / peak,
+           "peak_source": "%s hbm_gbs" % peak_src,
+           "bytes_per_probe_algorithmic": 64,
+           "dup_frac": float(flags.float().mean().item())}
+    eng.close()
+    del eng, d_off, d_tok
+    torch.cuda.empty_cache()
+    return res
+
+
 # --------------------------------------------------------------------------- GPU arm
 
 def main():
@@ -235,7 +295,8 @@ def main():
         eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n_total, cfg.fp_rate, cfg.seed, device=local,
                        sub_batch=args.sub_batch)
         sx = None
-        step = lambda o, t: eng.query_insert(o, t)  # noqa: E731
+        d_flags = torch.empty(args.docs, dtype=torch.uint8, device=dev)   # caller-owned output (no allocation per step)
+        step = lambda o, t: eng.query_insert(o, t, out=d_flags)  # noqa: E731
 
     def barrier():
         if world > 1:
@@ -251,6 +312,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     step_wall = []   # host wall time per step (diagnostic only: every call synchronises its stream)
+    step_stage = []  # with LSHBLOOM_BENCH_DIAG: per-step (reset wall ms, K1 ms, Bloom ms)
+    diag = bool(os.environ.get("LSHBLOOM_BENCH_DIAG"))
 
     def timed(fn, steps):
         barrier()
@@ -260,11 +323,19 @@ def main():
         e0.record(stream)
         out = None
         step_wall.clear()
+        step_stage.clear()
+        gc.collect()
+        gc.disable()   # a Python collection pause is not part of the GPU path
         for _ in range(steps):
             t0 = time.perf_counter()
             eng.reset()
+            t1 = time.perf_counter()
             out = fn()
             step_wall.append(1e3 * (time.perf_counter() - t0))
+            if diag:
+                (a, b), _ = eng.stage_times(enable=True)
+                step_stage.append((round(1e3 * (t1 - t0), 2), a, b))
+        gc.enable()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
@@ -272,7 +343,14 @@ def main():
 
     def wall_summary():
         w = sorted(step_wall)
-        return {"min": round(w[0], 3), "median": round(w[len(w) // 2], 3), "max": round(w[-1], 3)} if w else None
+        if not w:
+            return None
+        out = {"min": round(w[0], 3), "median": round(w[len(w) // 2], 3), "max": round(w[-1], 3)}
+        if diag:
+            med = w[len(w) // 2]
+            out["outliers"] = [(i, round(x, 2), [round(v, 2) for v in step_stage[i]] if i < len(step_stage) else None)
+                               for i, x in enumerate(step_wall) if x > 1.3 * med]
+        return out
 
     # ---- device-resident arm
     clk = ClockSampler(local)
@@ -301,7 +379,8 @@ def main():
             e2e_step = lambda: sx.query_insert(p_off.to(dev, non_blocking=True),  # noqa: E731
                                                p_tok.to(dev, non_blocking=True)).cpu()
         else:
-            e2e_step = lambda: eng.query_insert(p_off, p_tok)  # noqa: E731
+            h_flags = torch.empty(args.docs, dtype=torch.uint8).pin_memory()
+            e2e_step = lambda: eng.query_insert(p_off, p_tok, out=h_flags)  # noqa: E731
         for _ in range(max(1, args.warmup // 2)):
             eng.reset()
             e2e_step()
@@ -335,6 +414,11 @@ def main():
                 "evals_per_launch": evals, "ms_per_launch": k1_per_launch_ms,
                 "share_of_step": (k1_ms / max(1, args.steps)) / (ms / args.steps)}
 
+    bloom_hbm = None
+    if not args.no_hbm and world == 1:
+        del flags
+        bloom_hbm = hbm_leg(args, torch, dev, peaks, peak_src)
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         nthreads = os.cpu_count() or 1
@@ -360,6 +444,7 @@ def main():
                    "sub_batch": args.sub_batch or 32768, "csr_checksum_rank0": csum,
                    "dup_frac": dup_frac, "gen_s": round(gen_s, 1)},
         "roofline": roofline,
+        "roofline_bloom_hbm": bloom_hbm,
         "step_wall_ms": device_step_wall,
         "stages_ms_per_step": {"minhash_k1": k1_ms / max(1, args.steps), "bloom_k3_k6": bl_ms / max(1, args.steps)},
         "cpu_baseline": cpu,

@@ -54,6 +54,12 @@ __global__ void k(uint32_t* buf, uint64_t words, uint64_t n_threads, uint64_t sa
     for (int i = 0; i < 17; i++) v[i] = atomicOr(buf + pos[i], 1u << (i & 31));
 #pragma unroll
     for (int i = 0; i < 17; i++) acc |= v[i];
+  } else if (MODE == 6) {   // loads, then an unconditional atomic whose operand depends on the load
+    uint32_t v[17];
+#pragma unroll
+    for (int i = 0; i < 17; i++) v[i] = __ldcg(buf + pos[i]);
+#pragma unroll
+    for (int i = 0; i < 17; i++) acc |= atomicOr(buf + pos[i], 1u | (v[i] & 0x80000000u));
   } else {                  // MODE 5: loads, then atomics on every word (like K4 after a reload)
     uint32_t v[17];
 #pragma unroll
@@ -104,12 +110,13 @@ int main(int argc, char** argv) {
   cudaMalloc(&sink, 64);
   cudaMemset(buf, 0, words * 4);
   printf("{\"buffer_GB\": %.1f}\n", words * 4 / 1e9);
-  run<0>("load", buf, words, sink);
-  run<2>("atomicOr_noret", buf, words, sink);
-  run<1>("atomicOr_ret", buf, words, sink);
-  cudaMemset(buf, 0, words * 4);
-  run<3>("load_then_atomicOr", buf, words, sink);
-  run<4>("prefetchL2_then_atomicOr", buf, words, sink);
-  run<5>("load_then_atomicOr_all", buf, words, sink);
+  // every mode starts from an all-zero buffer
+  cudaMemset(buf, 0, words * 4); run<0>("load", buf, words, sink);
+  cudaMemset(buf, 0, words * 4); run<2>("atomicOr_noret", buf, words, sink);
+  cudaMemset(buf, 0, words * 4); run<1>("atomicOr_ret", buf, words, sink);
+  cudaMemset(buf, 0, words * 4); run<5>("load_then_atomicOr_all", buf, words, sink);
+  cudaMemset(buf, 0, words * 4); run<6>("load_then_atomicOr_dep", buf, words, sink);
+  cudaMemset(buf, 0, words * 4); run<3>("load_then_atomicOr_if_clear", buf, words, sink);
+  cudaMemset(buf, 0, words * 4); run<4>("prefetchL2_then_atomicOr", buf, words, sink);
   return 0;
 }
