@@ -213,13 +213,23 @@ def hbm_leg(args, torch, dev, peaks, peak_src):
     give the Bloom (K3-K6) time.  Algorithmic traffic per probe = one 32-B sector read + one
     32-B sector write-back; B200 moves a whole 128-B line per random access, which
     the measured random-access peak (tools/micro/rand_sector.cu) reflects."""
-    from paper_2411_04257_b200 import LSHBloom
     cfg = CONFIGS["C5"]
     n = args.hbm_docs
     off, tok = gen_range(cfg, 0, n)
     d_off = torch.from_numpy(off.view(np.int64)).to(dev)
     d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
-    eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=dev.index)
+    res = hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, "bloom")
+    # the blocked variant (SURVEY §8f NEXT #4): one 128-B line per (document, band)
+    res["blocked_variant"] = hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, "blocked")
+    del d_off, d_tok
+    torch.cuda.empty_cache()
+    return res
+
+
+def hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, index):
+    from paper_2411_04257_b200 import LSHBloom
+    n = d_off.numel() - 1
+    eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=dev.index, index=index)
     stream = torch.cuda.current_stream(dev)
     steps, warm = max(3, min(args.steps, 10)), 2
     tot = 0.0
@@ -240,19 +250,23 @@ def hbm_leg(args, torch, dev, peaks, peak_src):
     info = eng.info()
     probes = n * cfg.b * eng.k
     bl_step = bl_ms / max(1, bl_n)
-    alg_bytes = probes * 64.0
+    # standard: a 32-B sector read + write-back per probe; blocked: one 128-B line read +
+    # write-back per (document, band), i.e. 256 / k bytes per probe
+    bpp = 64.0 if index == "bloom" else 256.0 / eng.k
+    alg_bytes = probes * bpp
     peak = float(peaks.get("hbm_gbs", 6546.0))
-    res = {"bound": "hbm", "workload": "C5 geometry (128 perms, b=20 r=6, n_expected=1e9, %.1f GB filters), "
-                                      "first %d C5 documents per step, fresh filters" % (info["filter_bytes"] / 1e9, n),
+    res = {"bound": "hbm", "index": index,
+           "workload": "C5 geometry (128 perms, b=20 r=6, n_expected=1e9, %.1f GB filters), "
+                       "first %d C5 documents per step, fresh filters" % (info["filter_bytes"] / 1e9, n),
            "docs_per_s": n * steps / (tot / 1e3), "ms_per_step": tot / steps,
            "bloom_ms_per_step": bl_step, "probes_per_step": probes,
            "Gprobe_per_s": probes / bl_step / 1e6,
            "achieved": alg_bytes / bl_step / 1e6, "peak": peak, "unit": "GB/s", "frac": alg_bytes / bl_step / 1e6 / peak,
            "peak_source": "%s hbm_gbs" % peak_src,
-           "bytes_per_probe_algorithmic": 64,
+           "bytes_per_probe_algorithmic": round(bpp, 3),
            "dup_frac": float(flags.float().mean().item())}
     eng.close()
-    del eng, d_off, d_tok
+    del eng
     torch.cuda.empty_cache()
     return res
 
@@ -316,16 +330,16 @@ def main():
     diag = bool(os.environ.get("LSHBLOOM_BENCH_DIAG"))
 
     def timed(fn, steps):
+        step_wall.clear()
+        step_stage.clear()
+        gc.collect()
+        gc.disable()   # a Python collection pause is not part of the GPU path
         barrier()
         torch.cuda.synchronize(dev)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         out = None
-        step_wall.clear()
-        step_stage.clear()
-        gc.collect()
-        gc.disable()   # a Python collection pause is not part of the GPU path
         for _ in range(steps):
             t0 = time.perf_counter()
             eng.reset()
@@ -335,9 +349,9 @@ def main():
             if diag:
                 (a, b), _ = eng.stage_times(enable=True)
                 step_stage.append((round(1e3 * (t1 - t0), 2), a, b))
-        gc.enable()
         e1.record(stream)
         torch.cuda.synchronize(dev)
+        gc.enable()
         barrier()
         return e0.elapsed_time(e1), out
 

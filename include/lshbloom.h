@@ -96,8 +96,8 @@ typedef struct {
     uint32_t world;      /*   over world ranks (bands split as evenly as possible) */
     uint32_t sub_batch;  /* documents per Bloom sub-batch (0 = default 32768); results do
                             not depend on it */
-    uint32_t index_kind; /* LSHBLOOM_INDEX_BLOOM (0, the paper's method) or
-                            LSHBLOOM_INDEX_CLASSIC (1, see below) */
+    uint32_t index_kind; /* LSHBLOOM_INDEX_BLOOM (0, the paper's method),
+                            LSHBLOOM_INDEX_CLASSIC (1) or LSHBLOOM_INDEX_BLOCKED (2); see below */
 } lshbloom_config;
 
 /* Index kinds.
@@ -112,6 +112,17 @@ typedef struct {
  *   save/load return error 1. */
 #define LSHBLOOM_INDEX_BLOOM 0
 #define LSHBLOOM_INDEX_CLASSIC 1
+/* LSHBLOOM_INDEX_BLOCKED: a blocked Bloom variant (not the paper's filter,
+ *   whose layout SPEC S:328 leaves open): each filter is nb = ceil(m / 1024) blocks of 1024
+ *   bits (one 128-byte line, the unit B200 moves from HBM per random access) and all k probes
+ *   of a band hash fall in one block: block = h1 mod nb, offset_t = bits [10 (t mod 6),
+ *   10 (t mod 6) + 10) of mix64(h2 + floor(t / 6)), position = 1024 block + offset_t (h1, h2 as
+ *   for the standard filter, DESIGN R10).  m, k from (n_expected, fp_rate) as for the standard
+ *   filter, m rounded up to whole blocks; same stream semantics, 1 random line per (document,
+ *   band) instead of k.  Its false-positive rate at capacity is the Poisson mixture
+ *   sum_i Pois(i; n/nb) (1 - (1 - 1/1024)^(k i))^k (3.4x p at p = 1e-5, k = 17): ask for a
+ *   smaller fp_rate to compensate.  save/load return error 1. */
+#define LSHBLOOM_INDEX_BLOCKED 2
 
 typedef struct {
     uint64_t m;               /* bits per filter (analytic, the probe modulus) */
@@ -126,7 +137,7 @@ typedef struct {
     uint64_t seed;
     uint64_t n_expected;
     double fp_rate;
-    uint32_t index_kind;      /* LSHBLOOM_INDEX_BLOOM / _CLASSIC */
+    uint32_t index_kind;      /* LSHBLOOM_INDEX_BLOOM / _CLASSIC / _BLOCKED */
     uint64_t classic_slots;   /* classic: table slots per band (0 for Bloom) */
 } lshbloom_info_t;
 

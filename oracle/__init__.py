@@ -70,6 +70,10 @@ def _load():
                                        ctypes.POINTER(u64)]
         lib.orc_index_new.restype = vp
         lib.orc_index_new.argtypes = [u32, u64, dbl, u64]
+        lib.orc_index_new2.restype = vp
+        lib.orc_index_new2.argtypes = [u32, u64, dbl, u64, i32]
+        lib.orc_probes_blocked.restype = None
+        lib.orc_probes_blocked.argtypes = [u64, u64, u64, u64, u32, vp]
         lib.orc_index_free.restype = None
         lib.orc_index_free.argtypes = [vp]
         lib.orc_index_m.restype = u64
@@ -163,6 +167,13 @@ def probes(bh: int, s1: int, s2: int, m: int, k: int) -> np.ndarray:
     return g
 
 
+def probes_blocked(bh: int, s1: int, s2: int, nb: int, k: int) -> np.ndarray:
+    """Blocked variant: k positions inside one 1024-bit block (SURVEY §8f NEXT #4)."""
+    g = np.zeros(k, np.uint64)
+    _load().orc_probes_blocked(bh, s1, s2, nb, k, _ptr(g))
+    return g
+
+
 class OracleError(Exception):
     def __init__(self, code: int, msg: str):
         super().__init__(msg)
@@ -193,9 +204,10 @@ def signatures(offsets, tokens, num_perm: int, seed: int, *, b: int = 0, r: int 
 class Index:
     """The LSHBloom index of b Bloom filters, stream-order semantics."""
 
-    def __init__(self, b: int, n_expected: int, fp_rate: float, seed: int):
+    def __init__(self, b: int, n_expected: int, fp_rate: float, seed: int, blocked: bool = False):
         self._lib = _load()
-        self._h = self._lib.orc_index_new(b, n_expected, fp_rate, seed & (2**64 - 1))
+        self._h = self._lib.orc_index_new2(b, n_expected, fp_rate, seed & (2**64 - 1), 1 if blocked else 0)
+        self.blocked = blocked
         if not self._h:
             raise ValueError("orc_index_new: bad parameters")
         self.b = b

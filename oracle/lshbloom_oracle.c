@@ -148,6 +148,23 @@ void orc_probes(uint64_t bh, uint64_t s1, uint64_t s2, uint64_t m, uint32_t k, u
     for (uint32_t t = 0; t < k; t++) g[t] = (uint64_t)(((u128)h1 + (u128)t * (u128)h2) % (u128)m);
 }
 
+/* Blocked variant (SPEC S:328 leaves the filter layout open): the
+ * filter is nb blocks of 1024 bits (one 128-byte line) and all k probes of a band hash fall
+ * in one block:  block = h1 mod nb;  offsets are the 10-bit fields of w_j = mix64(h2 + j):
+ * o_t = (w_{t / 6} >> (10 (t mod 6))) & 1023;  g_t = 1024 * block + o_t,  t < k.
+ * h1, h2 as for the standard filter.  Offsets are independent and uniform (they may repeat,
+ * as positions of the standard filter may). */
+#define ORC_BLOCK_BITS 1024u
+void orc_probes_blocked(uint64_t bh, uint64_t s1, uint64_t s2, uint64_t nb, uint32_t k, uint64_t *g) {
+    uint64_t h1 = orc_mix64(bh ^ s1);
+    uint64_t h2 = orc_mix64(bh ^ s2) | 1ull;
+    uint64_t block = h1 % nb;
+    for (uint32_t t = 0; t < k; t++) {
+        uint64_t w = orc_mix64(h2 + t / 6);
+        g[t] = block * ORC_BLOCK_BITS + ((w >> (10 * (t % 6))) & (ORC_BLOCK_BITS - 1));
+    }
+}
+
 /* ------------------------------------------------------------------------ */
 /* Signatures + band hashes over a CSR batch, threads over documents.        */
 
@@ -212,16 +229,24 @@ int orc_signatures(uint64_t n_docs, const uint64_t *offsets, const uint32_t *tok
 
 typedef struct {
     uint32_t b, k;
+    int blocked;           /* 0: standard filter; 1: blocked variant (orc_probes_blocked) */
+    uint64_t nb;           /* blocked: number of 1024-bit blocks */
     uint64_t m, n_expected, doc_count;
     uint64_t seed;
     uint64_t *s1, *s2;
     uint8_t **bits; /* b arrays of ceil(m/8) bytes */
 } orc_index;
 
-void *orc_index_new(uint32_t b, uint64_t n_expected, double fp_rate, uint64_t seed) {
+/* blocked = 1: the standard m rounded up to whole 1024-bit blocks, same k. */
+void *orc_index_new2(uint32_t b, uint64_t n_expected, double fp_rate, uint64_t seed, int blocked) {
     uint64_t m; uint32_t k;
     if (b == 0 || orc_bloom_size(n_expected, fp_rate, &m, &k)) return NULL;
     orc_index *X = calloc(1, sizeof(orc_index));
+    if (blocked) {
+        X->blocked = 1;
+        X->nb = (m + ORC_BLOCK_BITS - 1) / ORC_BLOCK_BITS;
+        m = X->nb * ORC_BLOCK_BITS;
+    }
     X->b = b; X->k = k; X->m = m; X->n_expected = n_expected; X->seed = seed;
     X->s1 = malloc(8 * (size_t)b); X->s2 = malloc(8 * (size_t)b);
     orc_family(seed, 0, 0, b, NULL, NULL, NULL, NULL, X->s1, X->s2);
@@ -231,6 +256,10 @@ void *orc_index_new(uint32_t b, uint64_t n_expected, double fp_rate, uint64_t se
         if (!X->bits[j]) return NULL;
     }
     return X;
+}
+
+void *orc_index_new(uint32_t b, uint64_t n_expected, double fp_rate, uint64_t seed) {
+    return orc_index_new2(b, n_expected, fp_rate, seed, 0);
 }
 
 void orc_index_free(void *p) {
@@ -264,7 +293,8 @@ static void *orc_band_worker(void *arg) {
     uint8_t *F = X->bits[J->j];
     uint64_t *g = malloc(8 * (size_t)X->k);
     for (uint64_t i = 0; i < J->n_docs; i++) {
-        orc_probes(J->bh[i * J->ncol + J->col], X->s1[J->j], X->s2[J->j], X->m, X->k, g);
+        if (X->blocked) orc_probes_blocked(J->bh[i * J->ncol + J->col], X->s1[J->j], X->s2[J->j], X->nb, X->k, g);
+        else orc_probes(J->bh[i * J->ncol + J->col], X->s1[J->j], X->s2[J->j], X->m, X->k, g);
         int all = 1;                                          /* query: all k bits set */
         for (uint32_t t = 0; t < X->k; t++) all &= orc_get_bit(F, g[t]);
         for (uint32_t t = 0; t < X->k; t++) orc_set_bit(F, g[t]);   /* insert */

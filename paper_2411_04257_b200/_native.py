@@ -129,12 +129,13 @@ class LSHBloom:
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, shingle_n: int = 5, device: int | None = None, rank: int = 0, world: int = 1,
                  sub_batch: int = 0, index: str = "bloom", _handle=None):
-        """index: "bloom" (the paper's per-band Bloom filters) or "classic" (the exact
-        band-equality MinHashLSH index it replaces; fp_rate is ignored)."""
+        """index: "bloom" (the paper's per-band Bloom filters), "classic" (the exact
+        band-equality MinHashLSH index it replaces; fp_rate is ignored) or "blocked" (a blocked
+        Bloom variant: all k probes of a band hash in one 1024-bit block)."""
         self._lib = lib()
-        kinds = {"bloom": 0, "classic": 1}
+        kinds = {"bloom": 0, "classic": 1, "blocked": 2}
         if index not in kinds:
-            raise ValueError("index must be 'bloom' or 'classic'")
+            raise ValueError("index must be 'bloom', 'classic' or 'blocked'")
         if device is None:
             try:
                 import torch
@@ -155,7 +156,7 @@ class LSHBloom:
         self.device = device
         self.m, self.k = inf["m"], inf["k"]
         self.band_lo, self.band_hi = inf["band_lo"], inf["band_hi"]
-        self.index = "classic" if inf["index_kind"] == 1 else "bloom"
+        self.index = {0: "bloom", 1: "classic", 2: "blocked"}[inf["index_kind"]]
 
     # ------------------------------------------------------------------ plumbing
     def close(self):

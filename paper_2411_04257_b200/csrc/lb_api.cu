@@ -45,6 +45,7 @@ uint64_t R(uint64_t seed, uint64_t dom, uint64_t i) { return mix64(seed + kGamma
 struct lshbloom {
   lshbloom_config cfg{};
   uint64_t m = 0, m_inv = 0, W = 0;
+  uint64_t nb = 0, nb_inv = 0;    // blocked variant: 1024-bit blocks per band
   uint32_t k = 0, band_lo = 0, band_hi = 0, bl = 0, npl = 0, sub_batch = 0;
   int device = 0, sm_count = 148;
   cudaStream_t own_stream = nullptr, copy_stream = nullptr, bloom_stream = nullptr;
@@ -377,6 +378,8 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
   p.W = h->W;
   p.m = h->m;
   p.m_inv = h->m_inv;
+  p.nb = h->nb;
+  p.nb_inv = h->nb_inv;
   p.k = h->k;
   p.bl = h->bl;
   p.s1 = h->d_s1;
@@ -557,7 +560,8 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   if (c.r == 0 || (uint64_t)c.b * c.r > c.num_perm) return fail(nullptr, LSHBLOOM_EUSAGE, "need r >= 1 and b*r <= num_perm (S:183)");
   if (c.shingle_n == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "shingle_n must be >= 1");
   if (c.n_expected == 0) return fail(nullptr, LSHBLOOM_EUSAGE, "n_expected must be >= 1");
-  if (c.index_kind > LSHBLOOM_INDEX_CLASSIC) return fail(nullptr, LSHBLOOM_EUSAGE, "index_kind must be 0 (Bloom) or 1 (classic)");
+  if (c.index_kind > LSHBLOOM_INDEX_BLOCKED)
+    return fail(nullptr, LSHBLOOM_EUSAGE, "index_kind must be 0 (Bloom), 1 (classic) or 2 (blocked Bloom)");
   const bool classic = c.index_kind == LSHBLOOM_INDEX_CLASSIC;
   if (!classic && !(c.fp_rate > 0.0 && c.fp_rate < 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "fp_rate must be in (0, 1) (S:273)");
   if (c.world == 0) c.world = 1;
@@ -577,6 +581,11 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   h->cfg = c;
   h->m = (uint64_t)md;
   h->k = (uint32_t)kk;
+  if (c.index_kind == LSHBLOOM_INDEX_BLOCKED) {   // m rounded up to whole 1024-bit blocks
+    h->nb = (h->m + 1023) / 1024;
+    h->nb_inv = ~0ull / h->nb;
+    h->m = h->nb * 1024;
+  }
   h->m_inv = ~0ull / h->m;
   h->W = 2 * ((h->m + 63) / 64);
   const uint32_t base = c.b / c.world, rem = c.b % c.world;
@@ -847,7 +856,7 @@ int lshbloom_filter_copy(lshbloom* h, uint32_t j, uint32_t* dst) {
   int rc = check_handle(h);
   if (rc) return rc;
   if (!dst || j < h->band_lo || j >= h->band_hi) return fail(h, LSHBLOOM_EUSAGE, "band not owned by this handle / NULL dst");
-  if (h->cfg.index_kind != LSHBLOOM_INDEX_BLOOM) return fail(h, LSHBLOOM_EUSAGE, "not a Bloom index");
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) return fail(h, LSHBLOOM_EUSAGE, "not a Bloom index");
   DeviceGuard g(h->device);
   LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
   LB_CUDA(h, cudaMemcpy(dst, h->d_F + (uint64_t)(j - h->band_lo) * h->W, h->W * 4, cudaMemcpyDeviceToHost));
@@ -1040,7 +1049,7 @@ int lshbloom_save(lshbloom* h, const char* path) {
   if (rc) return rc;
   if (!path) return fail(h, LSHBLOOM_EUSAGE, "NULL path");
   if (h->cfg.world != 1) return fail(h, LSHBLOOM_EUSAGE, "save needs an unsharded handle (world = 1)");
-  if (h->cfg.index_kind != LSHBLOOM_INDEX_BLOOM) return fail(h, LSHBLOOM_EUSAGE, "save: not a Bloom index");
+  if (h->cfg.index_kind != LSHBLOOM_INDEX_BLOOM) return fail(h, LSHBLOOM_EUSAGE, "save: SPEC's LBF1 format holds standard Bloom filters only");
   if (h->cfg.shingle_n != 5) return fail(h, LSHBLOOM_EUSAGE, "the LSHB format carries no shingle width; save needs n = 5");
   DeviceGuard g(h->device);
   LB_CUDA(h, cudaDeviceSynchronize());

@@ -151,11 +151,33 @@ struct ProbeGen {   // sequential positions (any k)
   }
 };
 
-template <int KT, typename PT>   // KT > 0: all k positions in registers (PT = u32 when m <= 2^32)
-struct Probes {
+// Blocked variant (index_kind = LSHBLOOM_INDEX_BLOCKED): all k probes of a
+// band hash in one 1024-bit block (one 128-byte line, the unit B200 moves per random access):
+// block = h1 mod nb; offset_t = 10-bit field (t mod 6) of mix64(h2 + t / 6).
+struct BlockedGen {
+  uint64_t base, h2, w;
+  uint32_t t;
+  __device__ __forceinline__ BlockedGen(const BloomParams& p, uint64_t bh, uint32_t jl) {
+    const uint64_t h1 = mix64(bh ^ p.s1[jl]);
+    h2 = mix64(bh ^ p.s2[jl]) | 1ull;
+    base = mod_m(h1, p.nb, p.nb_inv) << 10;
+    t = 0;
+    w = 0;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint32_t f = t % 6;
+    if (f == 0) w = mix64(h2 + t / 6);
+    t++;
+    LB_ASSERT(base + ((w >> (10 * f)) & 1023u) < (uint64_t)1024 * 0x7FFFFFFFFull);
+    return base + ((w >> (10 * f)) & 1023u);
+  }
+};
+
+template <int KT, typename PT, typename GEN = ProbeGen>   // KT > 0: all k positions in registers
+struct Probes {                                           // (PT = u32 when m <= 2^32)
   PT g[KT];
   __device__ __forceinline__ Probes(const BloomParams& p, uint64_t bh, uint32_t jl) {
-    ProbeGen gen(p, bh, jl);
+    GEN gen(p, bh, jl);
 #pragma unroll
     for (int t = 0; t < KT; t++) g[t] = (PT)gen.next();
   }
@@ -164,7 +186,7 @@ struct Probes {
 __device__ __forceinline__ uint64_t full_mask(uint32_t k) { return k == 64 ? ~0ull : ((1ull << k) - 1); }
 
 // K3: probe positions + pre-sub-batch test.
-template <int KT, typename PT>
+template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
@@ -175,14 +197,14 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
   uint64_t pre = 0;
   if constexpr (KT > 0) {
-    const Probes<KT, PT> pr(p, bh, jl);
+    const Probes<KT, PT, GEN> pr(p, bh, jl);
     uint32_t w[KT];
 #pragma unroll
     for (int t = 0; t < KT; t++) w[t] = __ldcg(F + (pr.g[t] >> 5));   // all loads in flight
 #pragma unroll
     for (int t = 0; t < KT; t++) pre |= (uint64_t)((w[t] >> (pr.g[t] & 31)) & 1u) << t;
   } else {
-    ProbeGen gen(p, bh, jl);
+    GEN gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
       const uint64_t g = gen.next();
       pre |= (uint64_t)((__ldcg(F + (g >> 5)) >> (g & 31)) & 1u) << t;
@@ -193,7 +215,7 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
 }
 
 // K4: insert pre-unset probes; detect contested positions.
-template <int KT, typename PT>
+template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
@@ -214,7 +236,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
     }
   };
   if constexpr (KT > 0) {
-    const Probes<KT, PT> pr(p, bh, jl);
+    const Probes<KT, PT, GEN> pr(p, bh, jl);
     uint32_t old[KT];
 #pragma unroll
     for (int t = 0; t < KT; t++)         // all atomics in flight before any result is used
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
     for (int t = 0; t < KT; t++)
       if (!((pre >> t) & 1)) settle(t, pr.g[t], old[t]);
   } else {
-    ProbeGen gen(p, bh, jl);
+    GEN gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
       const uint64_t g = gen.next();
       if (!((pre >> t) & 1)) settle(t, g, atomicOr(F + (g >> 5), 1u << (g & 31)));
@@ -233,7 +255,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
 }
 
 // K5: first arrivals consult C; contested ones join E; sole probers make the band miss.
-template <int KT, typename PT>
+template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
@@ -246,7 +268,7 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   if (arr) {
     const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
     // (not early-exiting: every contested first arrival must join E for the other docs)
-    ProbeGen gen(p, bh, jl);
+    GEN gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
       const uint64_t g = gen.next();
       if ((arr >> t) & 1)
@@ -260,7 +282,7 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
 }
 
 // K6: verdict for candidate (doc, band) pairs.
-template <int KT, typename PT>
+template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
   if (*p.err) return;
   const uint32_t nc = *p.cand_count;
@@ -271,7 +293,7 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
     const uint32_t jl = idx / p.nsb;
     const uint32_t i = p.i0 + idx % p.nsb;
     const uint64_t pre = p.st_pre[idx];
-    ProbeGen gen(p, p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si], jl);
+    GEN gen(p, p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si], jl);
     bool hit = true;
     for (uint32_t t = 0; t < p.k && hit; t++) {
       const uint64_t g = gen.next();
@@ -282,12 +304,12 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
 
 }
 
-template <int KT, typename PT>
+template <int KT, typename PT, typename GEN = ProbeGen>
 static void launch_k(const BloomParams& p, unsigned grid, int sm_count, cudaStream_t s) {
-  k3_probe<KT, PT><<<grid, BL_THREADS, 0, s>>>(p);
-  k4_insert<KT, PT><<<grid, BL_THREADS, 0, s>>>(p);
-  k5_resolve<KT, PT><<<grid, BL_THREADS, 0, s>>>(p);
-  k6_verdict<KT, PT><<<(unsigned)sm_count * 2, BL_THREADS, 0, s>>>(p);
+  k3_probe<KT, PT, GEN><<<grid, BL_THREADS, 0, s>>>(p);
+  k4_insert<KT, PT, GEN><<<grid, BL_THREADS, 0, s>>>(p);
+  k5_resolve<KT, PT, GEN><<<grid, BL_THREADS, 0, s>>>(p);
+  k6_verdict<KT, PT, GEN><<<(unsigned)sm_count * 2, BL_THREADS, 0, s>>>(p);
 }
 
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
@@ -295,6 +317,15 @@ int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
   const unsigned grid = (unsigned)((n + BL_THREADS - 1) / BL_THREADS);
   cudaMemsetAsync(p.cand_count, 0, sizeof(uint32_t), s);
   cudaMemsetAsync(p.Q, 0xFF, 8ull << p.q_log2, s);   // this sub-batch's E: all slots empty
+  if (p.nb) {                                           // blocked variant
+    if (p.k == 17) {
+      if (p.m <= (1ull << 32)) launch_k<17, uint32_t, BlockedGen>(p, grid, sm_count, s);
+      else launch_k<17, uint64_t, BlockedGen>(p, grid, sm_count, s);
+    } else {
+      launch_k<0, uint64_t, BlockedGen>(p, grid, sm_count, s);
+    }
+    return 4;
+  }
   if (p.k == 17) {                                      // every BASELINE config (p = 1e-5)
     if (p.m <= (1ull << 32)) launch_k<17, uint32_t>(p, grid, sm_count, s);
     else launch_k<17, uint64_t>(p, grid, sm_count, s);   // C5: m = 23,962,645,944

@@ -46,14 +46,21 @@ __device__ __forceinline__ uint64_t affine32_mod_p(uint64_t c, uint32_t s, uint6
 
 // Per-permutation coefficients in the kernel's limb layout: a = a1 * 2^31 + a0 (a0 < 2^31,
 // a1 < 2^30) and b = b1 * 2^32 + b0 (see the MinHash evaluations in lb_minhash.cu).
+// Field order: a0 / a1 land in an even / odd register of the LDG.128 quad and b0 / b1 in an odd /
+// even one, so the 3-input adds ptxas forms from the two products and b (IADD3 on the low words,
+// IADD3.X on the high words) read registers from both banks.
 struct __align__(16) PermCoef {
-  uint32_t a0, a1, b0, b1;
+  uint32_t a0, a1, b1, b0;
 };
 
 // x = fingerprint mod P split for the eval: xl = x mod 2^30, xh = x >> 30 (< 2^31),
-// xh2 = 2 xh, xl4 = 4 xl (both < 2^32).
+// xh2 = 2 xh, xl4 = 4 xl (both < 2^32).  Field order matters: an LDS.128 fills an aligned
+// register quad, and PermCoef's a0 / a1 land in an even / odd register, so with xh, xl, xl4,
+// xh2 in that order every product a0*xl, a1*xh, a0*xh2, a1*xl4 reads one even- and one
+// odd-numbered register -- no register-bank conflict on the IMAD.WIDE (tools/micro/k1_loop.cu:
+// +9-10 % evaluations per clock over the xl, xh, xh2, xl4 order).
 struct __align__(16) XLimbs {
-  uint32_t xl, xh, xh2, xl4;
+  uint32_t xh, xl, xl4, xh2;
 };
 
 // Exact 64-bit h mod m with a precomputed inv = floor((2^64-1)/m) (Barrett; corrected).

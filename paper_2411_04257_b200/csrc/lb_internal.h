@@ -44,6 +44,7 @@ struct BloomParams {
   uint32_t q_log2;
   uint64_t W;                // uint32 words per band
   uint64_t m, m_inv;         // probe modulus and Barrett reciprocal
+  uint64_t nb, nb_inv;       // blocked variant: 1024-bit blocks per band and Barrett reciprocal
   uint32_t k, bl;            // probes, owned bands
   const uint64_t* s1;        // [bl] filter seeds of the owned bands (global band index)
   const uint64_t* s2;

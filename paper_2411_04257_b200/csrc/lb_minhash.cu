@@ -37,7 +37,7 @@ namespace lb {
 #define K1_WARPS (K1_THREADS / 32)
 
 // Coefficients: a = a1 2^31 + a0 (a0 < 2^31, a1 < 2^30), b = b1 2^32 + b0 (b < P), stored per
-// permutation as PermCoef{a0, a1, b0, b1}; shingle x = xh 2^30 + xl with xh2 = 2 xh, xl4 = 4 xl.
+// permutation as PermCoef{a0, a1, b1, b0}; shingle x = xh 2^30 + xl with xh2 = 2 xh, xl4 = 4 xl.
 //   a x = a1 xh 2^61 + 2^30 (a0 xh + 2 a1 xl) + a0 xl,   2^61 = 1 (mod P)
 //   A = a0 xl + a1 xh + b (< 3 2^61),  G = a0 xh2 + a1 xl4 (< 2^64),  2^30 (G/2) = G_hi + G_lo 2^29
 //   S = A + G_hi + G_lo 2^29 = a x + b (mod P),  0 <= S < 2^63 + 2^61

@@ -24,3 +24,13 @@ def test_parity_cases_under_device_asserts():
                           os.path.join(ROOT, "tests", "test_gpu_parity.py")],
                          env=env, cwd=ROOT, capture_output=True, text=True, timeout=1500)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+def test_blocked_cases_under_device_asserts():
+    from paper_2411_04257_b200 import build
+    build.build(checked=True)
+    env = dict(os.environ, LSHBLOOM_LIB=build.LIB_CHECKED)
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", "dense or sub_batch",
+                          os.path.join(ROOT, "tests", "test_gpu_blocked.py")],
+                         env=env, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]

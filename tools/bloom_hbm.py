@@ -4,7 +4,7 @@ Band hashes come from K1 over C5's first documents; steps after the first reuse 
 documents under a different hash seed (fresh band hashes with the same duplicate structure), so
 the filter keeps filling like a stream.  Reports ms per 1M-document step, probes/s and the
 algorithmic bytes/s (32 B sector read per probe + 32 B write-back per newly set bit).
-Usage: python tools/bloom_hbm.py [docs=1000000] [steps=4] [sub_batch,...=0] [n_expected=1e9]
+Usage: python tools/bloom_hbm.py [docs=1000000] [steps=4] [sub_batch,...=0] [n_expected=1e9] [bloom|blocked]
 """
 import json
 import os
@@ -23,6 +23,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 sbs = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0]
 n_expected = int(float(sys.argv[4])) if len(sys.argv) > 4 else CONFIGS["C5"].n_docs
+kind = sys.argv[5] if len(sys.argv) > 5 else "bloom"
 off, tok = gen_range(cfg, 0, n)
 dev = torch.device("cuda:0")
 d_off = torch.from_numpy(off.view(np.int64)).to(dev)
@@ -34,7 +35,8 @@ for s in range(steps + 1):
     del h
 torch.cuda.synchronize()
 for sb in sbs:
-    idx = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n_expected, cfg.fp_rate, cfg.seed, device=0, sub_batch=sb)
+    idx = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n_expected, cfg.fp_rate, cfg.seed, device=0, sub_batch=sb,
+                   index=kind)
     info = idx.info()
     idx.query_insert_bands(bhs[0])           # warm-up (also fills a little)
     res = []
@@ -45,7 +47,7 @@ for sb in sbs:
         probes = n * cfg.b * idx.k
         res.append({"step": s, "ms": round(ms, 3), "Gprobe_per_s": round(probes / ms / 1e6, 3),
                     "flagged": int(hits.sum().item())})
-    print(json.dumps({"sub_batch": sb, "filters_GB": info["filter_bytes"] / 1e9, "m": info["m"], "k": info["k"],
+    print(json.dumps({"index": kind, "sub_batch": sb, "filters_GB": info["filter_bytes"] / 1e9, "m": info["m"], "k": info["k"],
                       "docs": n, "probes_per_step": n * cfg.b * idx.k, "steps": res}), flush=True)
     idx.close()
     del idx

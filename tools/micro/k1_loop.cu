@@ -5,6 +5,7 @@
 //   MODE 1: no flag
 //   MODE 2: only the four IMAD.WIDE products folded into the minimum (not a valid result)
 //   MODE 3: exact carry-chain eval + min
+//   MODE 4-6: noflag with a register shift amount / without the quotient term / sums only
 // Reports evaluations / clock / SMSP (clock from clock64 inside the kernel).
 #include <cstdint>
 #include <cstdio>
@@ -12,9 +13,13 @@
 
 struct __align__(16) PermCoef { uint32_t a0, a1, b0, b1; };
 struct __align__(16) XLimbs { uint32_t xl, xh, xh2, xl4; };
+// Same limbs, reordered so that every product reads one even- and one odd-numbered register
+// (a0 / a1 sit in an even / odd register of the LDG.128 quad; LDS.128 fills an aligned quad).
+struct __align__(16) XLimbsB { uint32_t xh, xl, xl4, xh2; };
+__device__ uint32_t g_sh29 = 29;
 
-template <int MODE>
-__device__ __forceinline__ uint32_t ev(const PermCoef& c, const XLimbs& x, uint32_t& f) {
+template <int MODE, typename XL>
+__device__ __forceinline__ uint32_t ev(const PermCoef& c, const XL& x, uint32_t& f) {
   uint32_t y;
   if (MODE == 0 || MODE == 1) {
     asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1, t2;\n\t"
@@ -32,6 +37,31 @@ __device__ __forceinline__ uint32_t ev(const PermCoef& c, const XLimbs& x, uint3
         : "=r"(y)
         : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
     f = 0;
+  } else if (MODE == 4) {   // noflag with the shift amount in a register (SHF + IADD3 on the ALU pipe)
+    asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1, t2;\n\t"
+        "mov.b64 B, {%2, %3};\n\tmad.wide.u32 A, %1, %4, B;\n\tmad.wide.u32 A, %5, %6, A;\n\t"
+        "mul.wide.u32 G, %1, %7;\n\tmad.wide.u32 G, %5, %8, G;\n\tmov.b64 {s0, s1}, A;\n\tmov.b64 {g0, g1}, G;\n\t"
+        "shl.b32 t1, g0, %9;\n\tshr.u32 t2, g0, 3;\n\tadd.u32 s0, s0, t1;\n\tadd.u32 s0, s0, g1;\n\t"
+        "add.u32 s1, s1, t2;\n\tshr.u32 t1, s1, 29;\n\tadd.u32 %0, s0, t1;\n\t}"
+        : "=r"(y)
+        : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4), "r"(g_sh29));
+    f = 0;
+  } else if (MODE == 5) {   // noflag without the quotient term (y = low32(S); not a valid result)
+    asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1;\n\t"
+        "mov.b64 B, {%2, %3};\n\tmad.wide.u32 A, %1, %4, B;\n\tmad.wide.u32 A, %5, %6, A;\n\t"
+        "mul.wide.u32 G, %1, %7;\n\tmad.wide.u32 G, %5, %8, G;\n\tmov.b64 {s0, s1}, A;\n\tmov.b64 {g0, g1}, G;\n\t"
+        "shl.b32 t1, g0, 29;\n\tadd.u32 s0, s0, t1;\n\tadd.u32 %0, s0, g1;\n\t}"
+        : "=r"(y)
+        : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
+    f = 0;
+  } else if (MODE == 6) {   // four products, both 64-bit sums, no fold (y = A_lo ^ G_hi)
+    asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1;\n\t"
+        "mov.b64 B, {%2, %3};\n\tmad.wide.u32 A, %1, %4, B;\n\tmad.wide.u32 A, %5, %6, A;\n\t"
+        "mul.wide.u32 G, %1, %7;\n\tmad.wide.u32 G, %5, %8, G;\n\tmov.b64 {s0, s1}, A;\n\tmov.b64 {g0, g1}, G;\n\t"
+        "add.u32 %0, s0, g1;\n\t}"
+        : "=r"(y)
+        : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4));
+    f = 0;
   } else {
     asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1, t2, q;\n\t"
         "mov.b64 B, {%2, %3};\n\tadd.u64 B, B, 1;\n\tmad.wide.u32 A, %1, %4, B;\n\tmad.wide.u32 A, %5, %6, A;\n\t"
@@ -46,12 +76,18 @@ __device__ __forceinline__ uint32_t ev(const PermCoef& c, const XLimbs& x, uint3
   return y;
 }
 
-template <int MODE, int THREADS>
+template <int MODE, int THREADS, typename XL = XLimbs>
 __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, const XLimbs* __restrict__ X, int reps,
                                                 uint32_t* out, unsigned long long* cyc) {
-  __shared__ XLimbs xs[THREADS / 32][32];
+  __shared__ XL xs[THREADS / 32][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  xs[w][lane] = X[(blockIdx.x * 7 + w * 3 + lane) & 1023];
+  {
+    const XLimbs v = X[(blockIdx.x * 7 + w * 3 + lane) & 1023];
+    xs[w][lane].xl = v.xl;
+    xs[w][lane].xh = v.xh;
+    xs[w][lane].xh2 = v.xh2;
+    xs[w][lane].xl4 = v.xl4;
+  }
   PermCoef c[4];
 #pragma unroll
   for (int q = 0; q < 4; q++) c[q] = C[lane + 32 * q];
@@ -60,7 +96,7 @@ __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, 
   const unsigned long long t0 = clock64();
   for (int r = 0; r < reps; r++) {
     for (int j = 0; j < 32; j += 4) {
-      XLimbs xv[4];
+      XL xv[4];
 #pragma unroll
       for (int u = 0; u < 4; u++) xv[u] = xs[w][(j + u + r) & 31];   // varies per rep: no hoisting
 #pragma unroll
@@ -68,7 +104,7 @@ __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, 
 #pragma unroll
         for (int u = 0; u < 4; u += 2) {
           uint32_t f0, f1;
-          const uint32_t y0 = ev<MODE>(c[q], xv[u], f0), y1 = ev<MODE>(c[q], xv[u + 1], f1);
+          const uint32_t y0 = ev<MODE>(c[q], xv[u], f0), y1 = ev<MODE>(c[q], xv[u + 1], f1);  // NOLINT
           m[q] = min(m[q], min(y0, y1));
           if (MODE == 0) fmax = max(fmax, max(f0, f1));
         }
@@ -82,7 +118,7 @@ __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, 
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int MODE, int THREADS>
+template <int MODE, int THREADS, typename XL = XLimbs>
 void run(const char* name, int blocks_per_sm, const PermCoef* dC, const XLimbs* dX, uint32_t* dO,
          unsigned long long* dcyc) {
   const int reps = 2000, nb = 148 * blocks_per_sm;
@@ -92,7 +128,7 @@ void run(const char* name, int blocks_per_sm, const PermCoef* dC, const XLimbs* 
   float best = 1e9f;
   for (int r = 0; r < 4; r++) {
     cudaEventRecord(e0);
-    kern<MODE, THREADS><<<nb, THREADS>>>(dC, dX, reps, dO, dcyc);
+    kern<MODE, THREADS, XL><<<nb, THREADS>>>(dC, dX, reps, dO, dcyc);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -137,5 +173,11 @@ int main() {
   for (int bps : {2, 4}) run<1, 256>("noflag", bps, dC, dX, dO, dcyc);
   for (int bps : {2, 4}) run<2, 256>("wide_only", bps, dC, dX, dO, dcyc);
   for (int bps : {2, 4}) run<3, 256>("exact_chain", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<4, 256>("noflag_varshift", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<5, 256>("noflag_noq", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<6, 256>("wide_sums_only", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 3, 4}) run<0, 256, XLimbsB>("prod_banked", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<1, 256, XLimbsB>("noflag_banked", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<3, 256, XLimbsB>("exact_chain_banked", bps, dC, dX, dO, dcyc);
   return 0;
 }
