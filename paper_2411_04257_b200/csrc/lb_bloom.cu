@@ -151,6 +151,24 @@ struct ProbeGen {   // sequential positions (any k)
   }
 };
 
+// The same progression in 32-bit arithmetic when m <= 2^32 (every config but C5): with
+// md = m - (h2 mod m), g + (h2 mod m) mod m = (g < md) ? g + dl : g - md  -- no overflow.
+struct ProbeGen32 {
+  uint32_t x, dl, md;
+  __device__ __forceinline__ ProbeGen32(const BloomParams& p, uint64_t bh, uint32_t jl) {
+    const uint64_t h1 = mix64(bh ^ p.s1[jl]);
+    const uint64_t h2 = mix64(bh ^ p.s2[jl]) | 1ull;
+    x = (uint32_t)mod_m(h1, p.m, p.m_inv);
+    dl = (uint32_t)mod_m(h2, p.m, p.m_inv);
+    md = (uint32_t)(p.m - dl);
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint32_t g = x;
+    x = g < md ? g + dl : g - md;
+    return g;
+  }
+};
+
 // Blocked variant (index_kind = LSHBLOOM_INDEX_BLOCKED): all k probes of a
 // band hash in one 1024-bit block (one 128-byte line, the unit B200 moves per random access):
 // block = h1 mod nb; offset_t = 10-bit field (t mod 6) of mix64(h2 + t / 6).
@@ -327,7 +345,7 @@ int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
     return 4;
   }
   if (p.k == 17) {                                      // every BASELINE config (p = 1e-5)
-    if (p.m <= (1ull << 32)) launch_k<17, uint32_t>(p, grid, sm_count, s);
+    if (p.m <= (1ull << 32)) launch_k<17, uint32_t, ProbeGen32>(p, grid, sm_count, s);
     else launch_k<17, uint64_t>(p, grid, sm_count, s);   // C5: m = 23,962,645,944
   } else {
     launch_k<0, uint64_t>(p, grid, sm_count, s);
