@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hbm", action="store_true", help="skip the HBM-resident Bloom leg (C5 geometry)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: band-hash / flag exchange over peer memory (default) or NCCL")
     ap.add_argument("--hbm-docs", type=int, default=1_000_000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
     return ap.parse_args()
@@ -302,7 +304,13 @@ def main():
 
     if world > 1:
         sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, n_total, cfg.fp_rate, cfg.seed,
-                             device=local, sub_batch=args.sub_batch)
+                             device=local, sub_batch=args.sub_batch, exchange=args.exchange)
+        if args.exchange == "p2p":
+            try:                              # symmetric-memory rendezvous; NCCL if unavailable
+                sx._p2p_buffers(args.docs * world, args.docs, dev)
+            except Exception as e:            # noqa: BLE001
+                print("p2p exchange unavailable (%s); using NCCL" % e, file=sys.stderr)
+                sx.exchange = args.exchange = "nccl"
         eng = sx.engine
         step = lambda o, t: sx.query_insert(o, t)  # noqa: E731
     else:
@@ -453,7 +461,8 @@ def main():
                                                                     int(cfg.dup_frac * 100), cfg.shingle_n),
                    "num_perm": cfg.num_perm, "b": cfg.b, "r": cfg.r, "fp_rate": cfg.fp_rate,
                    "n_expected": n_total, "docs_per_step": n_total, "tokens_per_rank": int(len(tok)),
-                   "parallelism": "band-sharded x%d" % world if world > 1 else "single GPU",
+                   "parallelism": ("band-sharded x%d, %s exchange" % (world, args.exchange)) if world > 1
+                                  else "single GPU",
                    "l2": "inputs %.0f MB > 126 MB L2; filters zeroed each step" % (tok.nbytes / 1e6),
                    "sub_batch": args.sub_batch or 32768, "csr_checksum_rank0": csum,
                    "dup_frac": dup_frac, "gen_s": round(gen_s, 1)},

@@ -180,6 +180,29 @@ LSHBLOOM_API int lshbloom_query_insert(lshbloom *h, const lshbloom_batch *batch,
 LSHBLOOM_API int lshbloom_query_insert_bands(lshbloom *h, const uint64_t *bh_owned, uint64_t n_docs,
                                 int32_t on_device, void *stream, uint8_t *hit_out);
 
+/* Band-sharded exchange over peer memory (world > 1 on GPUs with
+ * peer access, e.g. NVLink / NVSwitch via torch symmetric memory).  Instead of an owner-major
+ * local buffer + all-to-all + all-reduce:
+ *  lshbloom_band_hashes_to_peers: K1 over this rank's documents, whose first document is
+ *    global_doc0 of the global batch, stores each band hash straight into its owner's receive
+ *    buffer: peer_recv[o] (a host array of `world` device pointers valid in this process, e.g.
+ *    symmetric-memory peer pointers) holds [n_global][band_hi(o) - band_lo(o)] uint64 in global
+ *    document order, and band j of global document g goes to
+ *    peer_recv[o][g * (hi - lo) + (j - lo)] for the o owning j.  Synchronises its stream.
+ *  lshbloom_query_insert_bands_peers: once every rank's band hashes have landed (a barrier
+ *    between the two calls is the caller's), query-then-insert the owned bands for all n_global
+ *    documents (bh_owned: this rank's receive buffer, device) and raise each hit document's flag
+ *    directly in its home rank's buffer: document g with doc_start[r] <= g < doc_start[r+1]
+ *    (host array of world+1 entries, doc_start[0] = 0, doc_start[world] = n_global) sets
+ *    peer_flags[r][g - doc_start[r]] = 1 (every owner stores the same 1, so no reduction is
+ *    needed).  Flag buffers must be zeroed before the first writer runs (the caller's barrier).
+ *    Mutates the owned filters; synchronises its stream.
+ * Results are bit-identical to lshbloom_query_insert on one GPU. */
+LSHBLOOM_API int lshbloom_band_hashes_to_peers(lshbloom *h, const lshbloom_batch *batch, uint64_t global_doc0,
+                                               void *const *peer_recv);
+LSHBLOOM_API int lshbloom_query_insert_bands_peers(lshbloom *h, const uint64_t *bh_owned, uint64_t n_global,
+                                                   const uint64_t *doc_start, void *const *peer_flags, void *stream);
+
 /* Zero every owned filter and the document count (as right after create). */
 LSHBLOOM_API int lshbloom_reset(lshbloom *h);
 

@@ -58,7 +58,8 @@ EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloo
            "lshbloom_band_hashes", "lshbloom_band_hashes_sharded", "lshbloom_query_insert",
            "lshbloom_query_insert_bands", "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info",
            "lshbloom_stage_times", "lshbloom_save", "lshbloom_load", "lshbloom_last_error",
-           "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan")
+           "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan",
+           "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers")
 
 
 def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
@@ -87,9 +88,12 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     lib.lshbloom_optimal_params.argtypes = [ctypes.c_double, u32, ctypes.c_double, ctypes.c_double,
                                             ctypes.POINTER(u32), ctypes.POINTER(u32)]
     lib.lshbloom_plan.argtypes = [u64, ctypes.c_double, ctypes.c_double, u32, ctypes.POINTER(_Plan)]
+    lib.lshbloom_band_hashes_to_peers.argtypes = [vp, ctypes.POINTER(_Batch), u64, ctypes.POINTER(vp)]
+    lib.lshbloom_query_insert_bands_peers.argtypes = [vp, vp, u64, ctypes.POINTER(u64), ctypes.POINTER(vp), vp]
     lib.lshbloom_launch_count.restype = u64
     for f in EXPORTS:
-        if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan"):
+        if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan",
+           "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers"):
             getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -241,6 +245,27 @@ class LSHBloom:
         self._check(self._lib.lshbloom_query_insert_bands(self._h, p, n, dev, stream or None,
                                                           self._ptr(out)))
         return out
+
+    def band_hashes_to_peers(self, offsets, tokens, global_doc0: int, peer_recv, *, stream=None):
+        """K1 over this rank's documents with every band hash stored straight into its owner
+        rank's receive buffer (peer_recv: `world` device pointers, e.g. symmetric memory)."""
+        bt, keep, n, dev = self._batch(offsets, tokens, stream)
+        ptrs = (ctypes.c_void_p * len(peer_recv))(*[int(x) for x in peer_recv])
+        self._check(self._lib.lshbloom_band_hashes_to_peers(self._h, ctypes.byref(bt), int(global_doc0), ptrs))
+
+    def query_insert_bands_peers(self, bh_owned, doc_start, peer_flags, *, stream=None):
+        """Bloom stage of the owned bands for all documents of the global batch, raising each hit
+        document's flag in its home rank's buffer (peer_flags: `world` device pointers)."""
+        p, dev, keep = _raw(bh_owned, "bh_owned")
+        if not dev:
+            raise ValueError("bh_owned must be a device tensor")
+        n = int(doc_start[-1])
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(bh_owned.device).cuda_stream
+        starts = (ctypes.c_uint64 * len(doc_start))(*[int(x) for x in doc_start])
+        ptrs = (ctypes.c_void_p * len(peer_flags))(*[int(x) for x in peer_flags])
+        self._check(self._lib.lshbloom_query_insert_bands_peers(self._h, p, n, starts, ptrs, stream or None))
 
     def save(self, path: str):
         """Checkpoint the filters and document count (SPEC's LSHB / LBF1 container)."""

@@ -224,6 +224,13 @@ BandMap full_map(const lshbloom* h) {
   return m;
 }
 
+// Absolute store pointers of a local layout (peer layouts come with ptr[] already set).
+BandMap resolve_map(BandMap m, uint64_t* out, uint32_t b) {
+  for (uint32_t j = 0; j < b; j++)
+    if (m.ncol[j] && !m.ptr[j]) m.ptr[j] = out + m.blockstart[j] + m.col[j];
+  return m;
+}
+
 // Reset the error gate: flags = 0, gate = 0, first_empty = ~0.
 int reset_err(lshbloom* h, cudaStream_t s) {
   LB_CUDA(h, cudaMemsetAsync(h->d_err, 0, 8, s));
@@ -264,7 +271,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
   MinhashParams p = base_params(h);
   p.sig_out = sig_dev;
   p.bh_out = bh_dev;
-  p.map = map;
+  p.map = resolve_map(map, bh_dev, h->cfg.b);
   int rc = reset_err(h, s);
   if (rc) return rc;
   if (b->on_device) {
@@ -332,7 +339,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
 
 // Classic index (lb_classic.cu): KC1 + KC2 over batch documents [i_begin, i_end).
 int run_classic(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin,
-                uint64_t i_end, uint8_t* dup_dev, cudaStream_t s, bool first, bool last) {
+                uint64_t i_end, uint8_t* dup_dev, cudaStream_t s, bool first, bool last, const DupSink* peers) {
   ClassicParams p;
   memset(&p, 0, sizeof p);
   p.keys = h->d_ckeys;
@@ -345,7 +352,8 @@ int run_classic(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh
   p.bh_si = bh_si;
   p.i0 = (uint32_t)i_begin;
   p.n = (uint32_t)(i_end - i_begin);
-  p.dup = dup_dev;
+  if (peers) p.dup = *peers;
+  else p.dup.local = dup_dev;
   p.full = (int*)h->d_counters + 8;
   p.err = &h->d_err->pad;
   if (first) stage_begin(h, 1, s);
@@ -368,9 +376,9 @@ int classic_capacity(lshbloom* h, uint64_t n) {
 
 // K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
 int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin, uint64_t i_end,
-              uint8_t* dup_dev, cudaStream_t s, bool first = true, bool last = true) {
+              uint8_t* dup_dev, cudaStream_t s, bool first = true, bool last = true, const DupSink* peers = nullptr) {
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC)
-    return run_classic(h, bh_dev, bh_sj, bh_si, i_begin, i_end, dup_dev, s, first, last);
+    return run_classic(h, bh_dev, bh_sj, bh_si, i_begin, i_end, dup_dev, s, first, last, peers);
   BloomParams p;
   memset(&p, 0, sizeof p);
   p.F = h->d_F;
@@ -395,7 +403,8 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
   p.st_arr = h->d_st + SB * h->bl;
   p.cand = h->d_cand;
   p.cand_count = h->d_counters;
-  p.dup = dup_dev;
+  if (peers) p.dup = *peers;
+  else p.dup.local = dup_dev;
   p.err = &h->d_err->pad;
   if (first) stage_begin(h, 1, s);
   for (uint64_t i0 = i_begin; i0 < i_end; i0 += SB) {
@@ -447,7 +456,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   uint64_t* bh = (uint64_t*)h->bh.p;
   MinhashParams p = base_params(h);
   p.bh_out = bh;
-  p.map = owned_band_major_map(h, n);
+  p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
   int rc = reset_err(h, s);
   if (rc) return rc;
   uint64_t chunk_tokens = 0;
@@ -833,6 +842,60 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   if (!on_device) LB_CUDA(h, cudaMemcpyAsync(hit_out, dhit, n_docs, cudaMemcpyDeviceToHost, s));
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n_docs;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_band_hashes_to_peers(lshbloom* h, const lshbloom_batch* b, uint64_t global_doc0, void* const* peer_recv) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if ((rc = check_batch(h, b))) return rc;
+  const uint32_t world = h->cfg.world, nb = h->cfg.b, base = nb / world, rem = nb % world;
+  if (!peer_recv) return fail(h, LSHBLOOM_EUSAGE, "NULL peer_recv");
+  for (uint32_t o = 0; o < world; o++)
+    if (!peer_recv[o]) return fail(h, LSHBLOOM_EUSAGE, "NULL receive buffer of rank " + std::to_string(o));
+  BandMap m;
+  memset(&m, 0, sizeof m);
+  for (uint32_t o = 0; o < world; o++) {
+    const uint32_t lo = o * base + std::min(o, rem), cnt = base + (o < rem ? 1 : 0);
+    for (uint32_t j = lo; j < lo + cnt; j++) {
+      m.ncol[j] = cnt;
+      m.ptr[j] = (uint64_t*)peer_recv[o] + global_doc0 * cnt + (j - lo);   // owner's [n_global][cnt] buffer
+    }
+  }
+  DeviceGuard g(h->device);
+  cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
+  if ((rc = run_minhash(h, b, s, nullptr, (uint64_t*)peer_recv[0], m))) return rc;
+  return finish(h, s);
+}
+
+int lshbloom_query_insert_bands_peers(lshbloom* h, const uint64_t* bh_owned, uint64_t n_global, const uint64_t* doc_start,
+                                      void* const* peer_flags, void* stream) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  const uint32_t world = h->cfg.world;
+  if (!bh_owned || !doc_start || !peer_flags) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_owned / doc_start / peer_flags");
+  if (n_global == 0 || n_global > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_global must be in [1, 2^32)");
+  if (world > (uint32_t)kMaxPeers) return fail(h, LSHBLOOM_EUSAGE, "world > 64");
+  if (doc_start[0] != 0 || doc_start[world] != n_global)
+    return fail(h, LSHBLOOM_EUSAGE, "doc_start must run from 0 to n_global");
+  DupSink sink;
+  memset(&sink, 0, sizeof sink);
+  sink.npeers = world;
+  for (uint32_t r = 0; r < world; r++) {
+    if (doc_start[r + 1] < doc_start[r]) return fail(h, LSHBLOOM_EUSAGE, "doc_start must be non-decreasing");
+    if (doc_start[r + 1] > doc_start[r] && !peer_flags[r])
+      return fail(h, LSHBLOOM_EUSAGE, "NULL flag buffer of rank " + std::to_string(r));
+    sink.peer[r] = (uint8_t*)peer_flags[r];
+    sink.start[r] = doc_start[r];
+  }
+  sink.start[world] = doc_start[world];
+  if ((rc = classic_capacity(h, n_global))) return rc;
+  DeviceGuard g(h->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
+  if ((rc = reset_err(h, s))) return rc;
+  if ((rc = run_bloom(h, bh_owned, 1, h->bl, 0, n_global, nullptr, s, true, true, &sink))) return rc;
+  if ((rc = finish(h, s))) return rc;
+  h->doc_count += n_global;
   return LSHBLOOM_OK;
 }
 

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
   LB_ASSERT(jl < p.bl);
   const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
+  asm volatile("" : "+l"(F));   // opaque: keep the band's base in a register (no per-probe remat)
   uint64_t pre = 0;
   if constexpr (KT > 0) {
     const Probes<KT, PT, GEN> pr(p, bh, jl);
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
     }
   }
   p.st_pre[idx] = pre;
-  if (pre == full_mask(p.k)) p.dup[i] = 1;
+  if (pre == full_mask(p.k)) raise_dup(p.dup, i);
 }
 
 // K4: insert pre-unset probes; detect contested positions.
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   LB_ASSERT(jl < p.bl);
   const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   uint32_t* F = p.F + (uint64_t)jl * p.W;
+  asm volatile("" : "+l"(F));
   uint64_t arr = 0;
   auto settle = [&](uint32_t t, uint64_t g, uint32_t old) {
     const uint32_t bit = 1u << (g & 31);
@@ -317,7 +319,7 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
       const uint64_t g = gen.next();
       if (!((pre >> t) & 1)) hit = e_find(p, qkey(jl, g)) < i;
     }
-    if (hit) p.dup[i] = 1;
+    if (hit) raise_dup(p.dup, i);
   }
 
 }

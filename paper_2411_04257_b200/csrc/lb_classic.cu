@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(KC_THREADS) kc_verdict(const ClassicParams p) 
   for (uint64_t n = 0; n <= mask; n++, s = (s + 1) & mask) {
     const unsigned long long cur = __ldcg(keys + s);
     if (cur == key) {
-      if (__ldcg(vals + s) < p.doc_base + i) p.dup[i] = 1;   // an earlier document holds it
+      if (__ldcg(vals + s) < p.doc_base + i) raise_dup(p.dup, i);   // an earlier document holds it
       return;
     }
     LB_ASSERT(cur != ~0ull);                                 // KC1 inserted every key

@@ -10,12 +10,44 @@ namespace lb {
 constexpr int kMaxBands = 64;
 
 // Where the K1 epilogue writes band hash j of batch document d (d indexes the whole batch,
-// not the launch's chunk):  out[blockstart[j] + d * ncol[j] + col[j]]  (skip ncol[j] == 0)
+// not the launch's chunk):  ptr[j][d * ncol[j]]  (skip ncol[j] == 0).  The host builds ptr[j]
+// either inside one local output, bh_out + blockstart[j] + col[j], or inside the owner rank's
+// receive buffer in peer memory (lshbloom_band_hashes_to_peers), so the same epilogue stores
+// band hashes locally or straight across NVLink.
 struct BandMap {
   uint64_t blockstart[kMaxBands];
   uint32_t ncol[kMaxBands];
   uint32_t col[kMaxBands];
+  uint64_t* ptr[kMaxBands];
 };
+
+constexpr int kMaxPeers = 64;
+
+// Where a (document, band) hit raises its document's duplicate flag.  Local: dup[i] = 1.  Peer
+// mode (lshbloom_query_insert_bands_peers, world = npeers > 0): document i of the global batch
+// belongs to rank r with start[r] <= i < start[r + 1] and its flag lives in that rank's buffer
+// peer[r] (peer memory over NVLink), so the OR over band owners is done by the stores themselves
+// (every writer stores the same value 1) instead of an all-reduce.
+struct DupSink {
+  uint8_t* local;
+  uint32_t npeers;
+  uint8_t* peer[kMaxPeers];
+  uint64_t start[kMaxPeers + 1];
+};
+
+__device__ __forceinline__ void raise_dup(const DupSink& d, uint32_t i) {
+  if (d.npeers == 0) {
+    d.local[i] = 1;
+    return;
+  }
+  uint32_t lo = 0, hi = d.npeers;                 // largest r with start[r] <= i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (d.start[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  d.peer[lo][i - d.start[lo]] = 1;
+}
 
 struct MinhashParams {
   const uint64_t* offsets;   // batch offsets (device), n+1
@@ -59,7 +91,7 @@ struct BloomParams {
   uint64_t* st_arr;          //   and first-arrival probe mask (K4)
   uint32_t* cand;            // candidate (doc, band) pairs
   uint32_t* cand_count;
-  uint8_t* dup;              // [n] batch flags (OR over owned bands)
+  DupSink dup;               // [n] batch flags (OR over owned bands), local or in peer memory
   const int* err;
 };
 
@@ -71,7 +103,7 @@ struct ClassicParams {        // classic MinHashLSH index (lb_classic.cu)
   const uint64_t* bh;        // band hashes: owned band jl of doc i at bh[jl*bh_sj + i*bh_si]
   uint64_t bh_sj, bh_si;
   uint32_t i0, n;            // batch documents [i0, i0 + n)
-  uint8_t* dup;              // [batch] flags (OR over owned bands)
+  DupSink dup;               // [batch] flags (OR over owned bands), local or in peer memory
   int* full;                 // set if a probe sequence wrapped (cannot happen at load <= 0.9)
   const int* err;
 };

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
           acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][j * p.r + u], __ldg(p.bcoef + p.r + u));
           acc = acc >= kP ? acc - kP : acc;
         }
-        p.bh_out[p.map.blockstart[j] + (uint64_t)d * p.map.ncol[j] + p.map.col[j]] = acc;
+        p.map.ptr[j][(uint64_t)d * p.map.ncol[j]] = acc;
       }
       __syncwarp();
     }
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
           acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][jb * p.r + u], __ldg(p.bcoef + p.r + u));
           acc = acc >= kP ? acc - kP : acc;
         }
-        p.bh_out[p.map.blockstart[jb] + (uint64_t)d * p.map.ncol[jb] + p.map.col[jb]] = acc;
+        p.map.ptr[jb][(uint64_t)d * p.map.ncol[jb]] = acc;
       }
       __syncwarp();
     }

@@ -13,6 +13,12 @@ Per batch:
   5. each rank keeps its own documents' flags.
 Results are bit-identical for every world size.  The collectives are plumbing (torch /
 NCCL); every arithmetic step runs in the library's kernels.
+
+exchange="p2p" replaces steps 1-4 by stores into peer memory: K1's
+epilogue writes every band hash straight into its owner's receive buffer (torch symmetric
+memory over NVLink / NVSwitch; lshbloom_band_hashes_to_peers), and the Bloom kernels raise each
+hit document's flag directly in its home rank's flag buffer (lshbloom_query_insert_bands_peers),
+with three device-side barriers per batch and no all-to-all, all-reduce or pack pass.
 """
 from __future__ import annotations
 
@@ -30,7 +36,11 @@ def band_range(rank: int, world: int, b: int) -> tuple[int, int]:
 class ShardedLSHBloom:
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, group=None, device: int | None = None, sub_batch: int = 0, index: str = "bloom",
-                 engine=None):
+                 exchange: str = "nccl", engine=None):
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange = exchange
+        self._p2p = None
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -57,6 +67,8 @@ class ShardedLSHBloom:
         device = offsets.device
         n_local = offsets.numel() - 1
         counts = self._counts(n_local, device)
+        if self.exchange == "p2p":
+            return self._query_insert_p2p(offsets, tokens, counts, device)
         send = self.engine.band_hashes_sharded(offsets, tokens)          # owner-major, flat
         in_splits = [n_local * w for w in self.widths]
         out_splits = [c * self.bl for c in counts]
@@ -70,3 +82,39 @@ class ShardedLSHBloom:
 
     def reset(self):
         self.engine.reset()
+
+    # ------------------------------------------------------------------ peer-memory exchange
+    def _p2p_buffers(self, n_global: int, n_local_max: int, device):
+        """Symmetric receive / flag buffers (same size on every rank; every rank takes the same
+        decision because it sees the same all-gathered counts)."""
+        import torch.distributed._symmetric_memory as symm_mem
+        bl_max = max(self.widths)
+        cur = self._p2p
+        if cur is not None and cur["cap_g"] >= n_global and cur["cap_l"] >= n_local_max:
+            return cur
+        cap_g = max(n_global, (cur or {}).get("cap_g", 0))
+        cap_l = max(n_local_max, (cur or {}).get("cap_l", 0))
+        recv = symm_mem.empty(cap_g * bl_max, dtype=torch.int64, device=device)
+        flags = symm_mem.empty(cap_l, dtype=torch.uint8, device=device)
+        hr = symm_mem.rendezvous(recv, self.group if self.group is not None else dist.group.WORLD)
+        hf = symm_mem.rendezvous(flags, self.group if self.group is not None else dist.group.WORLD)
+        self._p2p = {"cap_g": cap_g, "cap_l": cap_l, "recv": recv, "flags": flags, "hr": hr, "hf": hf,
+                     "peer_recv": [int(x) for x in hr.buffer_ptrs], "peer_flags": [int(x) for x in hf.buffer_ptrs]}
+        return self._p2p
+
+    def _query_insert_p2p(self, offsets, tokens, counts, device):
+        n_local = counts[self.rank]
+        n_global = sum(counts)
+        starts = [0]
+        for c in counts:
+            starts.append(starts[-1] + c)
+        buf = self._p2p_buffers(n_global, max(counts), device)
+        buf["flags"][:n_local].zero_()
+        buf["hr"].barrier(channel=0)            # flags zeroed everywhere; last batch's readers done
+        if n_local:
+            self.engine.band_hashes_to_peers(offsets, tokens, starts[self.rank], buf["peer_recv"])
+        buf["hr"].barrier(channel=1)            # every band hash has landed in its owner's buffer
+        recv = buf["recv"][:n_global * self.bl].view(n_global, self.bl)
+        self.engine.query_insert_bands_peers(recv, starts, buf["peer_flags"])
+        buf["hr"].barrier(channel=2)            # every hit flag has landed at its home rank
+        return buf["flags"][:n_local].clone()
