@@ -65,7 +65,10 @@ struct lshbloom {
   uint64_t gen = 1;
   uint64_t* d_st = nullptr;       // 2 * sub_batch * bl
   uint32_t* d_cand = nullptr;     // sub_batch * bl
-  uint32_t* d_counters = nullptr; // [0] candidates, [1..2] K1 work counters
+  uint32_t* d_counters = nullptr; // [1..2] K1 work counters, [8] classic full, [12..13] Bloom candidates / contested
+  uint64_t* d_clist = nullptr;    // contested probes of a sub-batch (sub_batch * bl * k)
+  uint32_t* d_cb = nullptr;       // contested-position summary bits (2^cb_log2)
+  uint32_t cb_log2 = 26;            // 8 MB: ~0.2 % of first arrivals collide with a contested position
   ErrState* d_err = nullptr;
   DevBuf off, tok[2], bh, dup, sig;
   uint64_t doc_count = 0, launches = 0;
@@ -128,7 +131,7 @@ int check_handle(lshbloom* h) {
 
 void free_all(lshbloom* h) {
   auto F = [](void* p) { if (p) cudaFree(p); };
-  F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_ekey);
+  F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_clist); F(h->d_cb); F(h->d_ekey);
   F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p);
   for (int i = 0; i < 2; i++) {
@@ -402,7 +405,10 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
   p.st_pre = h->d_st;
   p.st_arr = h->d_st + SB * h->bl;
   p.cand = h->d_cand;
-  p.cand_count = h->d_counters;
+  p.cand_count = h->d_counters + 12;
+  p.clist = h->d_clist;
+  p.cb = h->d_cb;
+  p.cb_log2 = h->cb_log2;
   if (peers) p.dup = *peers;
   else p.dup.local = dup_dev;
   p.err = &h->d_err->pad;
@@ -716,6 +722,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaMemset(h->d_eval, 0, (8ull << lg)));
   CR(cudaMalloc(&h->d_st, 2ull * h->sub_batch * h->bl * 8));
   CR(cudaMalloc(&h->d_cand, (size_t)h->sub_batch * h->bl * 4));
+  CR(cudaMalloc(&h->d_clist, (size_t)h->sub_batch * h->bl * h->k * 8));
+  if (const char* e = getenv("LSHBLOOM_CB_LOG2")) h->cb_log2 = std::max(10, std::min(30, atoi(e)));
+  CR(cudaMalloc(&h->d_cb, 1ull << (h->cb_log2 - 3)));
   CR(cudaMalloc(&h->d_counters, 16 * 4));
   CR(cudaMemset(h->d_counters, 0, 16 * 4));
   CR(cudaMalloc(&h->d_err, sizeof(ErrState)));

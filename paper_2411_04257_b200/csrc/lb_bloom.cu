@@ -9,13 +9,15 @@
 //   K3 probe   : positions g_t = (h1 + t h2) mod m, read F_pre; all k set -> hit.
 //   K4 insert  : atomicOr every pre-unset probe.  The one atomic that sees the bit clear is the
 //                position's first arrival; every other arrival sees it set -> the position is
-//                contested: the arrival enters itself in E (earliest setter, atomicMin).
-//   K5 resolve : each first arrival looks its position up in E: if present (contested) it joins
-//                the minimum; if absent it is the position's sole prober, so its band misses
-//                (E[p] = i).  Bands whose every pre-unset probe is contested become candidates.
-//   K6 verdict : candidate hit <=> E[p] < i for every pre-unset probe p.  (The previous
-//                sub-batch's E buffer is reset by a memset queued before K3.)
-// E holds only contested positions.  Its primary form Q is a compact open-addressed table of
+//                contested: the arrival is queued (clist) and its position flagged in a small
+//                contested-position summary bitmap (cb).
+//   K5 resolve : queued contested probes enter E (earliest setter, atomicMin); first arrivals
+//                whose summary bit is set enter E too; a first arrival with a clear bit is its
+//                position's sole prober, so its band misses (E[p] = i).  Bands whose every
+//                pre-unset probe is contested become candidates.
+//   K6 verdict : candidate hit <=> E[p] < i for every pre-unset probe p.  (The sub-batch's E
+//                buffer and summary are cleared by memsets queued before K3.)
+// E holds the contested positions (and the rare summary collisions).  Its primary form Q is a compact open-addressed table of
 // packed u64 slots ((band, position) << 22 | doc - i0; atomicMin keeps the earliest doc), two
 // buffers alternating by sub-batch, small enough to stay L2-resident.  A key whose probe
 // sequence in Q is full (64 slots) lives in the overflow table instead -- consistently, since
@@ -40,6 +42,13 @@ constexpr int kQProbe = 64;
 __device__ __forceinline__ uint64_t qkey(uint32_t jl, uint64_t g) { return ((uint64_t)jl << 36) | g; }
 __device__ __forceinline__ uint64_t qslot(const BloomParams& p, uint64_t key) {
   return (key * 0xD6E8FEB86659FD93ull) >> (64 - p.q_log2);
+}
+
+// Contested-position summary: one bit per hash(band, position), set for every contested probe
+// (K4b).  A clear bit proves a position has a single prober in the sub-batch, so K5 decides most
+// first arrivals without a Q lookup; a hash collision only costs a lookup.
+__device__ __forceinline__ uint32_t cbit(const BloomParams& p, uint64_t key) {
+  return (uint32_t)((key * 0xC2B2AE3D27D4EB4Full) >> (64 - p.cb_log2));
 }
 
 // Insert-or-update: E[key] = max(E[key], tag).  Stale (older-generation) slots count as empty.
@@ -98,24 +107,6 @@ __device__ void e_add(const BloomParams& p, uint64_t key, uint32_t i) {
     }
   }
   e_upsert(p, (p.gen << 42) | key, (p.gen << 32) | (uint64_t)(~i));   // overflow table
-}
-
-// K5: if key is contested (present in E), join its minimum with doc i and return true.
-__device__ bool e_join(const BloomParams& p, uint64_t key, uint32_t i) {
-  const uint64_t packed = (key << 22) | (uint64_t)(i - p.i0);
-  const uint64_t mask = (1ull << p.q_log2) - 1;
-  uint64_t s = qslot(p, key);
-  for (int n = 0; n < kQProbe; n++, s = (s + 1) & mask) {
-    const uint64_t cur = __ldcg(p.Q + s);
-    if (cur == kQEmpty) return false;
-    if ((cur >> 22) == key) {
-      atomicMin((unsigned long long*)(p.Q + s), (unsigned long long)packed);
-      return true;
-    }
-  }
-  if (e_lookup(p, (p.gen << 42) | key) == 0xFFFFFFFFu) return false;
-  e_upsert(p, (p.gen << 42) | key, (p.gen << 32) | (uint64_t)(~i));
-  return true;
 }
 
 // K6: earliest setter of key (batch document index), ~0u if absent.
@@ -250,7 +241,13 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   auto settle = [&](uint32_t t, uint64_t g, uint32_t old) {
     const uint32_t bit = 1u << (g & 31);
     if (old & bit) {                     // someone else set it in this sub-batch: contested
-      e_add(p, qkey(jl, g), i);
+      // queued for K5 (entering E here would make whole warps wait on one lane's table walk)
+      const uint64_t key = qkey(jl, g);
+      const uint32_t c = atomicAdd(p.cand_count + 1, 1u);
+      LB_ASSERT(c < (uint64_t)p.nsb * p.bl * p.k);
+      p.clist[c] = (key << 22) | (uint64_t)(i - p.i0);
+      const uint32_t h = cbit(p, key);
+      atomicOr(p.cb + (h >> 5), 1u << (h & 31));
     } else {
       arr |= 1ull << t;                  // first arrival
     }
@@ -274,11 +271,25 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
   p.st_arr[idx] = arr;
 }
 
-// K5: first arrivals consult C; contested ones join E; sole probers make the band miss.
+// K5: (a) the contested probes K4 queued enter E; (b) every first arrival whose position is
+// flagged in the contested-position summary enters E too (insert-or-min, so the order of (a)
+// and (b) across threads does not matter; a summary collision only adds an entry that no other
+// document reads and that makes its own band miss, as a sole prober must).  A first arrival
+// with a clear summary bit is a sole prober: its band misses.  Bands whose first arrivals are
+// all flagged become candidates for K6.
 template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
   const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
+  if (*p.err) return;
+  {
+    const uint32_t nc = p.cand_count[1];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t c = idx; c < nc; c += stride) {
+      const uint64_t e = p.clist[c];
+      e_add(p, e >> 22, p.i0 + (uint32_t)(e & 0x3FFFFFull));
+    }
+  }
+  if (idx >= (uint64_t)p.nsb * p.bl) return;
   const uint64_t pre = p.st_pre[idx];
   if (pre == full_mask(p.k)) return;
   const uint64_t arr = p.st_arr[idx];
@@ -291,8 +302,12 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
     GEN gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
       const uint64_t g = gen.next();
-      if ((arr >> t) & 1)
-        if (!e_join(p, qkey(jl, g), i)) maybe = false;   // sole prober: not set before i
+      if ((arr >> t) & 1) {
+        const uint64_t key = qkey(jl, g);
+        const uint32_t h = cbit(p, key);
+        if (!((__ldg(p.cb + (h >> 5)) >> (h & 31)) & 1u)) maybe = false;   // sole prober
+        else e_add(p, key, i);                             // (possibly) contested: join E
+      }
     }
   }
   if (maybe) {
@@ -335,8 +350,9 @@ static void launch_k(const BloomParams& p, unsigned grid, int sm_count, cudaStre
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
   const uint64_t n = (uint64_t)p.nsb * p.bl;
   const unsigned grid = (unsigned)((n + BL_THREADS - 1) / BL_THREADS);
-  cudaMemsetAsync(p.cand_count, 0, sizeof(uint32_t), s);
+  cudaMemsetAsync(p.cand_count, 0, 2 * sizeof(uint32_t), s);   // candidates, contested probes
   cudaMemsetAsync(p.Q, 0xFF, 8ull << p.q_log2, s);   // this sub-batch's E: all slots empty
+  cudaMemsetAsync(p.cb, 0, 1ull << (p.cb_log2 - 3), s);
   if (p.nb) {                                           // blocked variant
     if (p.k == 17) {
       if (p.m <= (1ull << 32)) launch_k<17, uint32_t, BlockedGen>(p, grid, sm_count, s);

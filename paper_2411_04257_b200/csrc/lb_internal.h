@@ -90,7 +90,10 @@ struct BloomParams {
   uint64_t* st_pre;          // [nsb * bl] per (doc, band): pre-set probe mask (K3)
   uint64_t* st_arr;          //   and first-arrival probe mask (K4)
   uint32_t* cand;            // candidate (doc, band) pairs
-  uint32_t* cand_count;
+  uint32_t* cand_count;      //   and their count; cand_count[1] counts clist
+  uint64_t* clist;           // contested probes of the sub-batch, packed (band, position) << 22 | doc - i0
+  uint32_t* cb;              // contested-position summary: 2^cb_log2 bits, bit hash(band, position)
+  uint32_t cb_log2;
   DupSink dup;               // [n] batch flags (OR over owned bands), local or in peer memory
   const int* err;
 };

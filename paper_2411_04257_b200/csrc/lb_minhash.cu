@@ -108,6 +108,20 @@ __device__ __forceinline__ uint32_t eval_fast(const PermCoef& c, const XLimbs& x
 }
 
 
+// Token loads: read-only path, L1-allocating (each token is read by up to n lanes), and marked
+// evict-first in L2 -- the 0.8 GB of tokens a C2 batch streams through once must not push the
+// concurrently running Bloom kernels' filters (48 MB, L2-resident) out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint32_t ld_token(const uint32_t* ptr, uint64_t pol) {
+  uint32_t v;
+  asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+
 __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
   uint64_t x = mod_p(fp);
   XLimbs l;
@@ -124,6 +138,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
   __shared__ uint32_t sg[K1_WARPS][32 * NPL];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (*p.err) return;
+  const uint64_t tpol = l2_evict_first_policy();
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
@@ -152,7 +167,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
       const uint32_t s = s0 + lane;
       if (s < S) {
         uint64_t h = init;
-        for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)__ldg(tk + s + j));
+        for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
         xs[w][lane] = make_limbs(h);
       }
       __syncwarp();
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const Minha
         const uint32_t s = s0 + lane;
         if (s < S) {
           uint64_t h = init;
-          for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)__ldg(tk + s + j));
+          for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
           xs[w][lane] = make_limbs(h);
         }
         __syncwarp();
@@ -287,6 +302,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
   __shared__ uint32_t sg[K1_WARPS][32 * NPL];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (*p.err) return;
+  const uint64_t tpol = l2_evict_first_policy();
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
@@ -313,7 +329,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
       const uint32_t s = s0 + lane;
       if (s < S) {
         uint64_t h = init;
-        for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)__ldg(tk + s + j));
+        for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
         xs[w][lane] = make_limbs(h);
       }
       __syncwarp();

@@ -12,14 +12,15 @@
 #include <cuda_runtime.h>
 
 struct __align__(16) PermCoef { uint32_t a0, a1, b0, b1; };
+struct __align__(16) PermCoefB { uint32_t a0, a1, b1, b0; };   // the library's order
 struct __align__(16) XLimbs { uint32_t xl, xh, xh2, xl4; };
 // Same limbs, reordered so that every product reads one even- and one odd-numbered register
 // (a0 / a1 sit in an even / odd register of the LDG.128 quad; LDS.128 fills an aligned quad).
 struct __align__(16) XLimbsB { uint32_t xh, xl, xl4, xh2; };
 __device__ uint32_t g_sh29 = 29;
 
-template <int MODE, typename XL>
-__device__ __forceinline__ uint32_t ev(const PermCoef& c, const XL& x, uint32_t& f) {
+template <int MODE, typename XL, typename PC>
+__device__ __forceinline__ uint32_t ev(const PC& c, const XL& x, uint32_t& f) {
   uint32_t y;
   if (MODE == 0 || MODE == 1) {
     asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1, t2;\n\t"
@@ -46,6 +47,14 @@ __device__ __forceinline__ uint32_t ev(const PermCoef& c, const XL& x, uint32_t&
         : "=r"(y)
         : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4), "r"(g_sh29));
     f = 0;
+  } else if (MODE == 7) {   // production (with flag) but the shift amount in a register: SHF + IADD3 on ALU
+    asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1, t2;\n\t"
+        "mov.b64 B, {%3, %4};\n\tmad.wide.u32 A, %2, %5, B;\n\tmad.wide.u32 A, %6, %7, A;\n\t"
+        "mul.wide.u32 G, %2, %8;\n\tmad.wide.u32 G, %6, %9, G;\n\tmov.b64 {s0, s1}, A;\n\tmov.b64 {g0, g1}, G;\n\t"
+        "shl.b32 t1, g0, %10;\n\tshr.u32 t2, g0, 3;\n\tadd.u32 s0, s0, t1;\n\tadd.u32 s0, s0, g1;\n\t"
+        "add.u32 s1, s1, t2;\n\tor.b32 %1, s1, 0xE0000000;\n\tshr.u32 t1, s1, 29;\n\tadd.u32 %0, s0, t1;\n\t}"
+        : "=r"(y), "=r"(f)
+        : "r"(c.a0), "r"(c.b0), "r"(c.b1), "r"(x.xl), "r"(c.a1), "r"(x.xh), "r"(x.xh2), "r"(x.xl4), "r"(g_sh29));
   } else if (MODE == 5) {   // noflag without the quotient term (y = low32(S); not a valid result)
     asm("{\n\t.reg .u64 A, G, B;\n\t.reg .u32 s0, s1, g0, g1, t1;\n\t"
         "mov.b64 B, {%2, %3};\n\tmad.wide.u32 A, %1, %4, B;\n\tmad.wide.u32 A, %5, %6, A;\n\t"
@@ -76,7 +85,7 @@ __device__ __forceinline__ uint32_t ev(const PermCoef& c, const XL& x, uint32_t&
   return y;
 }
 
-template <int MODE, int THREADS, typename XL = XLimbs>
+template <int MODE, int THREADS, typename XL = XLimbs, typename PC = PermCoef>
 __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, const XLimbs* __restrict__ X, int reps,
                                                 uint32_t* out, unsigned long long* cyc) {
   __shared__ XL xs[THREADS / 32][32];
@@ -88,9 +97,15 @@ __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, 
     xs[w][lane].xh2 = v.xh2;
     xs[w][lane].xl4 = v.xl4;
   }
-  PermCoef c[4];
+  PC c[4];
 #pragma unroll
-  for (int q = 0; q < 4; q++) c[q] = C[lane + 32 * q];
+  for (int q = 0; q < 4; q++) {
+    const PermCoef v = C[lane + 32 * q];
+    c[q].a0 = v.a0;
+    c[q].a1 = v.a1;
+    c[q].b0 = v.b0;
+    c[q].b1 = v.b1;
+  }
   uint32_t m[4] = {~0u, ~0u, ~0u, ~0u}, fmax = 0;
   __syncwarp();
   const unsigned long long t0 = clock64();
@@ -106,7 +121,7 @@ __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, 
           uint32_t f0, f1;
           const uint32_t y0 = ev<MODE>(c[q], xv[u], f0), y1 = ev<MODE>(c[q], xv[u + 1], f1);  // NOLINT
           m[q] = min(m[q], min(y0, y1));
-          if (MODE == 0) fmax = max(fmax, max(f0, f1));
+          if (MODE == 0 || MODE == 7) fmax = max(fmax, max(f0, f1));
         }
     }
   }
@@ -118,7 +133,7 @@ __global__ void __launch_bounds__(THREADS) kern(const PermCoef* __restrict__ C, 
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-template <int MODE, int THREADS, typename XL = XLimbs>
+template <int MODE, int THREADS, typename XL = XLimbs, typename PC = PermCoef>
 void run(const char* name, int blocks_per_sm, const PermCoef* dC, const XLimbs* dX, uint32_t* dO,
          unsigned long long* dcyc) {
   const int reps = 2000, nb = 148 * blocks_per_sm;
@@ -128,7 +143,7 @@ void run(const char* name, int blocks_per_sm, const PermCoef* dC, const XLimbs* 
   float best = 1e9f;
   for (int r = 0; r < 4; r++) {
     cudaEventRecord(e0);
-    kern<MODE, THREADS, XL><<<nb, THREADS>>>(dC, dX, reps, dO, dcyc);
+    kern<MODE, THREADS, XL, PC><<<nb, THREADS>>>(dC, dX, reps, dO, dcyc);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -179,5 +194,8 @@ int main() {
   for (int bps : {2, 3, 4}) run<0, 256, XLimbsB>("prod_banked", bps, dC, dX, dO, dcyc);
   for (int bps : {2, 4}) run<1, 256, XLimbsB>("noflag_banked", bps, dC, dX, dO, dcyc);
   for (int bps : {2, 4}) run<3, 256, XLimbsB>("exact_chain_banked", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<0, 256, XLimbsB, PermCoefB>("prod_banked_bswap", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<7, 256, XLimbsB, PermCoefB>("prod_banked_bswap_varshift", bps, dC, dX, dO, dcyc);
+  for (int bps : {2, 4}) run<1, 256, XLimbsB, PermCoefB>("noflag_banked_bswap", bps, dC, dX, dO, dcyc);
   return 0;
 }
