@@ -197,10 +197,10 @@ __device__ __forceinline__ uint64_t full_mask(uint32_t k) { return k == 64 ? ~0u
 // K3: probe positions + pre-sub-batch test.
 template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
-  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
-  const uint32_t jl = (uint32_t)(idx / p.nsb);          // band-major: a wave touches few filters
-  const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
+  // grid (doc blocks, bands): blocks run x-fastest, so a wave works in one band's filter
+  const uint32_t il = blockIdx.x * blockDim.x + threadIdx.x, jl = blockIdx.y;
+  if (*p.err || il >= p.nsb) return;
+  const uint32_t idx = jl * p.nsb + il, i = p.i0 + il;
   LB_ASSERT(jl < p.bl);
   const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   const uint32_t* F = p.F + (uint64_t)jl * p.W;
@@ -227,12 +227,11 @@ __global__ void __launch_bounds__(BL_THREADS) k3_probe(const BloomParams p) {
 // K4: insert pre-unset probes; detect contested positions.
 template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
-  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (*p.err || idx >= (uint64_t)p.nsb * p.bl) return;
+  const uint32_t il = blockIdx.x * blockDim.x + threadIdx.x, jl = blockIdx.y;
+  if (*p.err || il >= p.nsb) return;
+  const uint32_t idx = jl * p.nsb + il, i = p.i0 + il;
   const uint64_t pre = p.st_pre[idx];
   if (pre == full_mask(p.k)) return;
-  const uint32_t jl = (uint32_t)(idx / p.nsb);          // band-major: a wave touches few filters
-  const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
   LB_ASSERT(jl < p.bl);
   const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   uint32_t* F = p.F + (uint64_t)jl * p.W;
@@ -279,40 +278,51 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
 // all flagged become candidates for K6.
 template <int KT, typename PT, typename GEN>
 __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
-  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t il = blockIdx.x * blockDim.x + threadIdx.x, jl = blockIdx.y;
   if (*p.err) return;
   {
     const uint32_t nc = p.cand_count[1];
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t c = idx; c < nc; c += stride) {
+    const uint32_t stride = gridDim.x * gridDim.y * blockDim.x;
+    for (uint32_t c = (blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; c < nc; c += stride) {
       const uint64_t e = p.clist[c];
       e_add(p, e >> 22, p.i0 + (uint32_t)(e & 0x3FFFFFull));
     }
   }
-  if (idx >= (uint64_t)p.nsb * p.bl) return;
+  if (il >= p.nsb) return;
+  const uint32_t idx = jl * p.nsb + il, i = p.i0 + il;
   const uint64_t pre = p.st_pre[idx];
   if (pre == full_mask(p.k)) return;
   const uint64_t arr = p.st_arr[idx];
-  const uint32_t jl = (uint32_t)(idx / p.nsb);
-  const uint32_t i = p.i0 + (uint32_t)(idx % p.nsb);
   bool maybe = true;
   if (arr) {
     const uint64_t bh = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
     // (not early-exiting: every contested first arrival must join E for the other docs)
+    // Flagged first arrivals are collected (up to 2 per lane) and entered in E after the scan
+    // with the warp's lanes together, rather than one divergent table walk per probe index.
+    uint64_t pk0 = 0, pk1 = 0;
+    uint32_t np = 0;
     GEN gen(p, bh, jl);
     for (uint32_t t = 0; t < p.k; t++) {
       const uint64_t g = gen.next();
       if ((arr >> t) & 1) {
         const uint64_t key = qkey(jl, g);
         const uint32_t h = cbit(p, key);
-        if (!((__ldg(p.cb + (h >> 5)) >> (h & 31)) & 1u)) maybe = false;   // sole prober
-        else e_add(p, key, i);                             // (possibly) contested: join E
+        if (!((__ldg(p.cb + (h >> 5)) >> (h & 31)) & 1u)) {
+          maybe = false;                                   // sole prober
+        } else {                                           // (possibly) contested: join E
+          if (np == 0) pk0 = key;
+          else if (np == 1) pk1 = key;
+          else e_add(p, key, i);
+          np++;
+        }
       }
     }
+    if (np > 0) e_add(p, pk0, i);
+    if (np > 1) e_add(p, pk1, i);
   }
   if (maybe) {
     const uint32_t c = atomicAdd(p.cand_count, 1u);
-    p.cand[c] = (uint32_t)idx;
+    p.cand[c] = idx;
   }
 }
 
@@ -340,7 +350,7 @@ __global__ void __launch_bounds__(BL_THREADS) k6_verdict(const BloomParams p) {
 }
 
 template <int KT, typename PT, typename GEN = ProbeGen>
-static void launch_k(const BloomParams& p, unsigned grid, int sm_count, cudaStream_t s) {
+static void launch_k(const BloomParams& p, dim3 grid, int sm_count, cudaStream_t s) {
   k3_probe<KT, PT, GEN><<<grid, BL_THREADS, 0, s>>>(p);
   k4_insert<KT, PT, GEN><<<grid, BL_THREADS, 0, s>>>(p);
   k5_resolve<KT, PT, GEN><<<grid, BL_THREADS, 0, s>>>(p);
@@ -348,8 +358,7 @@ static void launch_k(const BloomParams& p, unsigned grid, int sm_count, cudaStre
 }
 
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s) {
-  const uint64_t n = (uint64_t)p.nsb * p.bl;
-  const unsigned grid = (unsigned)((n + BL_THREADS - 1) / BL_THREADS);
+  const dim3 grid((p.nsb + BL_THREADS - 1) / BL_THREADS, p.bl);   // (doc blocks, bands)
   cudaMemsetAsync(p.cand_count, 0, 2 * sizeof(uint32_t), s);   // candidates, contested probes
   cudaMemsetAsync(p.Q, 0xFF, 8ull << p.q_log2, s);   // this sub-batch's E: all slots empty
   cudaMemsetAsync(p.cb, 0, 1ull << (p.cb_log2 - 3), s);

@@ -31,10 +31,11 @@ __device__ __forceinline__ uint64_t cslot(uint64_t key, uint32_t log2cap) {
 }
 
 __global__ void __launch_bounds__(KC_THREADS) kc_insert(const ClassicParams p) {
-  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (*p.err || idx >= (uint64_t)p.n * p.bl) return;
-  const uint32_t jl = (uint32_t)(idx / p.n);             // band-major: a wave works in few tables
-  const uint32_t i = p.i0 + (uint32_t)(idx % p.n);
+  // grid (doc blocks, bands): blocks run x-fastest, so a wave works in one band's table
+  const uint64_t il = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t jl = blockIdx.y;
+  if (*p.err || il >= p.n) return;
+  const uint32_t i = p.i0 + (uint32_t)il;
   const uint64_t key = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   const unsigned long long gdoc = p.doc_base + i;
   unsigned long long* keys = (unsigned long long*)p.keys + ((uint64_t)jl << p.log2cap);
@@ -57,10 +58,10 @@ __global__ void __launch_bounds__(KC_THREADS) kc_insert(const ClassicParams p) {
 }
 
 __global__ void __launch_bounds__(KC_THREADS) kc_verdict(const ClassicParams p) {
-  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (*p.err || idx >= (uint64_t)p.n * p.bl) return;
-  const uint32_t jl = (uint32_t)(idx / p.n);
-  const uint32_t i = p.i0 + (uint32_t)(idx % p.n);
+  const uint64_t il = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t jl = blockIdx.y;
+  if (*p.err || il >= p.n) return;
+  const uint32_t i = p.i0 + (uint32_t)il;
   const uint64_t key = p.bh[(uint64_t)jl * p.bh_sj + (uint64_t)i * p.bh_si];
   const unsigned long long* keys = (const unsigned long long*)p.keys + ((uint64_t)jl << p.log2cap);
   const unsigned long long* vals = (const unsigned long long*)p.vals + ((uint64_t)jl << p.log2cap);
@@ -78,8 +79,7 @@ __global__ void __launch_bounds__(KC_THREADS) kc_verdict(const ClassicParams p) 
 }
 
 int launch_classic(const ClassicParams& p, cudaStream_t s) {
-  const uint64_t n = (uint64_t)p.n * p.bl;
-  const unsigned grid = (unsigned)((n + KC_THREADS - 1) / KC_THREADS);
+  const dim3 grid((unsigned)(((uint64_t)p.n + KC_THREADS - 1) / KC_THREADS), p.bl);   // (doc blocks, bands)
   kc_insert<<<grid, KC_THREADS, 0, s>>>(p);
   kc_verdict<<<grid, KC_THREADS, 0, s>>>(p);
   return 2;
