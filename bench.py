@@ -436,6 +436,19 @@ def main():
                 "evals_per_launch": evals, "ms_per_launch": k1_per_launch_ms,
                 "share_of_step": (k1_ms / max(1, args.steps)) / (ms / args.steps)}
 
+    # K1 alone (lshbloom_band_hashes: one launch over the batch, the whole GPU, no Bloom
+    # kernels beside it) -- the kernel's own rate, next to its rate inside the overlapped step
+    if world == 1:
+        eng.band_hashes(d_off, d_tok)
+        eng.stage_times(enable=True)
+        for _ in range(3):
+            eng.band_hashes(d_off, d_tok)
+        (a_ms, _), (a_n, _) = eng.stage_times(enable=False)
+        if a_n:
+            roofline["alone_ms_per_launch"] = a_ms / a_n
+            roofline["alone_achieved"] = evals / (a_ms / a_n / 1e3) / 1e9
+            roofline["alone_frac"] = roofline["alone_achieved"] / roofline["peak"]
+
     bloom_hbm = None
     if not args.no_hbm and world == 1:
         del flags

@@ -287,7 +287,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
     p.counter = h->d_counters + 1;
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
     stage_begin(h, 0, s);
-    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, 0);   // K1 alone: whole GPU
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     stage_end(h, 0, s);
     h->launches += l;
@@ -328,7 +328,7 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
     p.n_docs = (uint32_t)(d1 - d0);
     p.counter = h->d_counters + 1 + buf;
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
-    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, 0);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     h->launches += l;
     LB_CUDA(h, cudaGetLastError());

@@ -132,8 +132,8 @@ __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
   return l;
 }
 
-template <int NPL, int UNR>
-__global__ void __launch_bounds__(K1_THREADS, LB_K1_MINB) k1_minhash(const MinhashParams p) {
+template <int NPL, int UNR, int MINB = LB_K1_MINB>
+__global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
   __shared__ uint32_t sg[K1_WARPS][32 * NPL];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -459,18 +459,18 @@ static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int ma
 }
 
 
-template <int NPL, int UNR>
+template <int NPL, int UNR, int MINB = LB_K1_MINB>
 static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR>, K1_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR, MINB>, K1_THREADS, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  k1_minhash<NPL, UNR><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  k1_minhash<NPL, UNR, MINB><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
@@ -496,7 +496,12 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
   switch (npl) {
     case 1: return launch_t<1, 4>(p, sm_count, s, max_bps);
     case 2: return launch_t<2, 4>(p, sm_count, s, max_bps);
-    case 4: return launch_t<4, LB_UNR4>(p, sm_count, s, max_bps);
+    // alone (max_bps == 0: signatures, band hashes, the sharded paths) K1 takes the whole GPU
+    // and a 64-register build runs 4 blocks per SM (1467 vs 1421 Geval/s on C2); beside the
+    // Bloom kernels (fused query_insert) the 92-register build at 2 blocks per SM leaves them
+    // room (19.6 vs 20.5+ ms per C2 step, tools/k1_variants.py + bench.py)
+    case 4: return max_bps == 0 ? launch_t<4, LB_UNR4, 4>(p, sm_count, s, 0)
+                                : launch_t<4, LB_UNR4>(p, sm_count, s, max_bps);
     case 8: return launch_t<8, 2>(p, sm_count, s, max_bps);
     case 16: return launch_t<16, 2>(p, sm_count, s, max_bps);
     case 32: return launch_t<32, 2>(p, sm_count, s, max_bps);
