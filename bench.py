@@ -228,6 +228,19 @@ def hbm_leg(args, torch, dev, peaks, peak_src):
     return res
 
 
+def hbm_traffic(index, probes):
+    """DRAM bytes per step (read + write) of the standard filter's Bloom stage from the committed
+    ncu capture (profiles/bloom_hbm_traffic_C5.json, per probe x probes per step): a random probe
+    moves a whole 128-B line for K3's read and again for K4's atomic."""
+    if index != "bloom":
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "bloom_hbm_traffic_C5.json")) as f:
+            return json.load(f)["dram_bytes_per_probe"] * probes
+    except Exception:
+        return None
+
+
 def hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, index):
     from paper_2411_04257_b200 import LSHBloom
     n = d_off.numel() - 1
@@ -266,6 +279,7 @@ def hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, index):
            "achieved": alg_bytes / bl_step / 1e6, "peak": peak, "unit": "GB/s", "frac": alg_bytes / bl_step / 1e6 / peak,
            "peak_source": "%s hbm_gbs" % peak_src,
            "bytes_per_probe_algorithmic": round(bpp, 3),
+           "traffic": hbm_traffic(index, probes),
            "dup_frac": float(flags.float().mean().item())}
     eng.close()
     del eng
