@@ -70,7 +70,7 @@ struct lshbloom {
   uint32_t* d_cb = nullptr;       // contested-position summary bits (2^cb_log2)
   uint32_t cb_log2 = 26;            // 8 MB: ~0.2 % of first arrivals collide with a contested position
   ErrState* d_err = nullptr;
-  DevBuf off, tok[2], bh, dup, sig;
+  DevBuf off, tok[2], bh, dup, sig, part;
   uint64_t doc_count = 0, launches = 0;
   // classic MinHashLSH index (index_kind = LSHBLOOM_INDEX_CLASSIC)
   uint64_t* d_ckeys = nullptr;    // [bl][2^c_log2cap]
@@ -133,7 +133,7 @@ void free_all(lshbloom* h) {
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_clist); F(h->d_cb); F(h->d_ekey);
   F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
-  F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p);
+  F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
   for (int i = 0; i < 2; i++) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
@@ -272,6 +272,11 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
                 uint64_t* bh_dev, const BandMap& map) {
   const uint64_t n = b->n_docs;
   MinhashParams p = base_params(h);
+  if (h->npl >= 8) {   // scratch of the length-partitioned K1 launches (lb_minhash.cu)
+    LB_CUDA(h, ensure(h->part, (2 * (size_t)b->n_docs + 2) * sizeof(uint32_t)));
+    p.part_lists = (uint32_t*)h->part.p;
+    p.part_counts = (uint32_t*)h->part.p + 2 * b->n_docs;
+  }
   p.sig_out = sig_dev;
   p.bh_out = bh_dev;
   p.map = resolve_map(map, bh_dev, h->cfg.b);
@@ -461,6 +466,11 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   const uint64_t n = b->n_docs;
   uint64_t* bh = (uint64_t*)h->bh.p;
   MinhashParams p = base_params(h);
+  if (h->npl >= 8) {   // scratch of the length-partitioned K1 launches (lb_minhash.cu)
+    LB_CUDA(h, ensure(h->part, (2 * (size_t)b->n_docs + 2) * sizeof(uint32_t)));
+    p.part_lists = (uint32_t*)h->part.p;
+    p.part_counts = (uint32_t*)h->part.p + 2 * b->n_docs;
+  }
   p.bh_out = bh;
   p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
   int rc = reset_err(h, s);

@@ -67,6 +67,12 @@ struct MinhashParams {
   const uint64_t* bcoef;     // c[0..r), d[0..r)
   BandMap map;
   const int* err;            // nonzero: batch rejected, do nothing
+  // Length-partitioned launches (npl >= 8): this launch handles batch documents list[0, *list_n)
+  // instead of [doc0, doc0 + n_docs); part_* is scratch for the partition (2 lists of n_docs).
+  const uint32_t* list;
+  const uint32_t* list_n;
+  uint32_t* part_lists;      // [2][n_docs]: short documents, long documents
+  uint32_t* part_counts;     // [2]
 };
 
 struct BloomParams {

@@ -147,8 +147,8 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashPara
     uint32_t di = 0;
     if (lane == 0) di = atomicAdd(p.counter, 1u);
     di = __shfl_sync(0xffffffffu, di, 0);
-    if (di >= p.n_docs) break;
-    const uint32_t d = p.doc0 + di;
+    if (di >= (p.list ? *p.list_n : p.n_docs)) break;
+    const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
     uint32_t di = 0;
     if (lane == 0) di = atomicAdd(p.counter, 1u);
     di = __shfl_sync(0xffffffffu, di, 0);
-    if (di >= p.n_docs) break;
-    const uint32_t d = p.doc0 + di;
+    if (di >= (p.list ? *p.list_n : p.n_docs)) break;
+    const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -474,6 +474,18 @@ static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int ma
   return 1;
 }
 
+// K1p: split this launch's documents into short (S < split_s shingles) and long ones.
+__global__ void k1_partition(const MinhashParams p, uint32_t split_s) {
+  const uint32_t di = blockIdx.x * blockDim.x + threadIdx.x;
+  if (*p.err || di >= p.n_docs) return;
+  const uint32_t d = p.doc0 + di;
+  const uint64_t L = p.offsets[d + 1] - p.offsets[d];
+  const uint64_t S = L >= p.shingle_n ? L - p.shingle_n + 1 : 1;
+  const int which = S >= split_s ? 1 : 0;
+  const uint32_t at = atomicAdd(p.part_counts + which, 1u);
+  p.part_lists[(uint64_t)which * p.n_docs + at] = d;
+}
+
 int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps) {
   // Kernel choice (measured on B200, tools/k1_variants.py): with 128 permutations (npl 4) the
   // exact kernel wins on abstract-length documents (C2: 1203 vs ~1100 Geval/s); with 256
@@ -483,6 +495,28 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
   if (mode < 0) {
     const char* e = getenv("LSHBLOOM_K1");
     mode = !e ? 2 : (e[0] == 'e' ? 0 : 1);
+  }
+  if (mode == 2 && npl == 8 && p.part_lists && p.n_docs > 0) {
+    // 256 permutations: the screened kernel wins on full-text lengths (C3: 1760 vs 1236 Geval/s)
+    // but loses on abstracts (C2 shapes: 680 vs 1269), so split each launch by length
+    // (C4 is 31M abstracts + 8M full texts) and run each part on its kernel.
+    static uint32_t split_s = 0;
+    if (!split_s) {
+      const char* e = getenv("LSHBLOOM_K1_SPLIT_S");
+      split_s = e ? (uint32_t)atoi(e) : 1024u;
+    }
+    cudaMemsetAsync(p.part_counts, 0, 2 * sizeof(uint32_t), s);
+    k1_partition<<<(p.n_docs + 255) / 256, 256, 0, s>>>(p, split_s);
+    MinhashParams a = p, b = p;
+    a.list = p.part_lists;
+    a.list_n = p.part_counts;
+    b.list = p.part_lists + p.n_docs;
+    b.list_n = p.part_counts + 1;
+    cudaMemsetAsync(p.counter, 0, 4, s);
+    launch_t<8, 2>(a, sm_count, s, max_bps);
+    cudaMemsetAsync(p.counter, 0, 4, s);
+    launch_s<8>(b, sm_count, s, max_bps);
+    return 3;
   }
   const bool screened = mode == 1 || (mode == 2 && npl >= 8);
   if (screened && npl <= 8) {

@@ -312,3 +312,34 @@ print("ok")
     env = dict(os.environ, LSHBLOOM_K1=mode, PYTHONPATH=root)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("split", ["1", "300", "100000"])
+def test_length_partitioned_k1(split):
+    # 256 permutations: each K1 launch is split by shingle count into an exact-kernel part and a
+    # screened-kernel part (lb_minhash.cu); every threshold must give the oracle's outputs,
+    # including all-long (1) and all-short (100000) partitions; subprocess because the
+    # threshold is read once per process
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle
+from synthetic.corpus import CONFIGS, gen_range
+from paper_2411_04257_b200 import LSHBloom
+for name, n in (("C4", 2000), ("C1", 1500)):
+    cfg = CONFIGS[name]
+    off, tok = gen_range(cfg, 0, n)
+    sig, bh, dup, _ = oracle.run(off, tok, num_perm=256, b=32, r=8, n_expected=n, fp_rate=1e-4, seed=3)
+    idx = LSHBloom(256, 32, 8, n, 1e-4, 3, device=0)
+    d = (torch.from_numpy(off.view(np.int64)).cuda(), torch.from_numpy(tok.view(np.int32)).cuda())
+    assert (idx.signatures(*d).cpu().numpy().view(np.uint32) == sig).all(), name
+    assert (idx.band_hashes(off, tok) == bh).all(), name
+    assert (idx.query_insert(*d).cpu().numpy() == dup).all(), name
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LSHBLOOM_K1_SPLIT_S=split, PYTHONPATH=root)
+    env.pop("LSHBLOOM_K1", None)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
