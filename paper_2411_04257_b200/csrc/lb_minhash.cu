@@ -132,10 +132,15 @@ __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
   return l;
 }
 
-template <int NPL, int UNR, int MINB = LB_K1_MINB>
+// PASSES > 1: the lane's 32 NPL PASSES permutations are evaluated NPL at a time, one pass over
+// the document's shingles each (coefficients reloaded per pass, the signature row collected in
+// shared memory for the band hashes): the register footprint of NPL permutations per lane for
+// PASSES x NPL of them -- 256 permutations on short documents at 4 per lane run at the 128-
+// permutation kernel's occupancy instead of the 8-per-lane kernel's.
+template <int NPL, int UNR, int MINB = LB_K1_MINB, int PASSES = 1>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
-  __shared__ uint32_t sg[K1_WARPS][32 * NPL];
+  __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (*p.err) return;
   const uint64_t tpol = l2_evict_first_policy();
@@ -158,6 +163,11 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashPara
     const uint32_t t = L >= n ? n : (uint32_t)L;
     const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
 
+    for (int pass = 0; pass < PASSES; pass++) {
+    if (PASSES > 1) {
+#pragma unroll
+      for (int q = 0; q < NPL; q++) c[q] = p.coef[pass * 32 * NPL + lane + 32 * q];
+    }
     uint32_t mn[NPL];
 #pragma unroll
     for (int q = 0; q < NPL; q++) mn[q] = 0xFFFFFFFFu;
@@ -224,13 +234,16 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashPara
     if (p.sig_out) {
 #pragma unroll
       for (int q = 0; q < NPL; q++) {
-        const uint32_t pm = lane + 32 * q;
+        const uint32_t pm = pass * 32 * NPL + lane + 32 * q;
         if (pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = mn[q];
       }
     }
     if (p.bh_out) {
 #pragma unroll
-      for (int q = 0; q < NPL; q++) sg[w][lane + 32 * q] = mn[q];
+      for (int q = 0; q < NPL; q++) sg[w][pass * 32 * NPL + lane + 32 * q] = mn[q];
+    }
+    }  // pass
+    if (p.bh_out) {
       __syncwarp();
       for (uint32_t j = lane; j < p.b; j += 32) {
         if (p.map.ncol[j] == 0) continue;
@@ -459,18 +472,18 @@ static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int ma
 }
 
 
-template <int NPL, int UNR, int MINB = LB_K1_MINB>
+template <int NPL, int UNR, int MINB = LB_K1_MINB, int PASSES = 1>
 static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR, MINB>, K1_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR, MINB, PASSES>, K1_THREADS, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  k1_minhash<NPL, UNR, MINB><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  k1_minhash<NPL, UNR, MINB, PASSES><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
@@ -513,7 +526,8 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     b.list = p.part_lists + p.n_docs;
     b.list_n = p.part_counts + 1;
     cudaMemsetAsync(p.counter, 0, 4, s);
-    launch_t<8, 2>(a, sm_count, s, max_bps);
+    if (max_bps == 0) launch_t<4, LB_UNR4, 4, 2>(a, sm_count, s, 0);   // 256 = 2 passes x 4 x 32
+    else launch_t<4, LB_UNR4, LB_K1_MINB, 2>(a, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8>(b, sm_count, s, max_bps);
     return 3;
