@@ -36,6 +36,11 @@
  * the streaming verdict against a brute-force set formulation and the classic
  * exact-band-equality index; Bloom FP / fill against their
  * analytic values.
+ *
+ * Parity unpinned (documented conventions whose exact values nothing outside
+ * this file fixes; pinned only by the properties listed in DESIGN.md §2):
+ * orc_fingerprint (DESIGN R1) and orc_probes_blocked's in-block offsets (the
+ * blocked variant, is this build's own definition).
  */
 #include <math.h>
 #include <pthread.h>
