@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-hbm", action="store_true", help="skip the HBM-resident Bloom leg (C5 geometry)")
+    ap.add_argument("--index", default="bloom", choices=["bloom", "classic", "blocked"],
+                    help="index kind: the paper's Bloom filters (default), the classic MinHashLSH "
+                         "index, or the blocked Bloom variant")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: band-hash / flag exchange over peer memory (default) or NCCL")
     ap.add_argument("--hbm-docs", type=int, default=1_000_000)
@@ -318,7 +321,7 @@ def main():
 
     if world > 1:
         sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, n_total, cfg.fp_rate, cfg.seed,
-                             device=local, sub_batch=args.sub_batch, exchange=args.exchange)
+                             device=local, sub_batch=args.sub_batch, exchange=args.exchange, index=args.index)
         if args.exchange == "p2p":
             try:                              # symmetric-memory rendezvous; NCCL if unavailable
                 sx._p2p_buffers(args.docs * world, args.docs, dev)
@@ -329,7 +332,7 @@ def main():
         step = lambda o, t: sx.query_insert(o, t)  # noqa: E731
     else:
         eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n_total, cfg.fp_rate, cfg.seed, device=local,
-                       sub_batch=args.sub_batch)
+                       sub_batch=args.sub_batch, index=args.index)
         sx = None
         d_flags = torch.empty(args.docs, dtype=torch.uint8, device=dev)   # caller-owned output (no allocation per step)
         step = lambda o, t: eng.query_insert(o, t, out=d_flags)  # noqa: E731
@@ -488,6 +491,7 @@ def main():
                                                                     int(cfg.dup_frac * 100), cfg.shingle_n),
                    "num_perm": cfg.num_perm, "b": cfg.b, "r": cfg.r, "fp_rate": cfg.fp_rate,
                    "n_expected": n_total, "docs_per_step": n_total, "tokens_per_rank": int(len(tok)),
+                   "index": args.index, "index_bytes": int(eng.info()["filter_bytes"]),
                    "parallelism": ("band-sharded x%d, %s exchange" % (world, args.exchange)) if world > 1
                                   else "single GPU",
                    "l2": "inputs %.0f MB > 126 MB L2; filters zeroed each step" % (tok.nbytes / 1e6),
