@@ -47,8 +47,9 @@ __device__ __forceinline__ uint64_t qslot(const BloomParams& p, uint64_t key) {
 // Contested-position summary: one bit per hash(band, position), set for every contested probe
 // (K4b).  A clear bit proves a position has a single prober in the sub-batch, so K5 decides most
 // first arrivals without a Q lookup; a hash collision only costs a lookup.
-__device__ __forceinline__ uint32_t cbit(const BloomParams& p, uint64_t key) {
-  return (uint32_t)((key * 0xC2B2AE3D27D4EB4Full) >> (64 - p.cb_log2));
+__device__ __forceinline__ uint32_t cbit(const BloomParams& p, uint32_t jl, uint64_t g) {
+  const uint32_t x = ((uint32_t)g ^ (uint32_t)(g >> 32)) * 0x9E3779B1u + jl * 0x85EBCA77u;
+  return (x * 0xC2B2AE35u) >> (32 - p.cb_log2);
 }
 
 // Insert-or-update: E[key] = max(E[key], tag).  Stale (older-generation) slots count as empty.
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(BL_THREADS) k4_insert(const BloomParams p) {
       const uint32_t c = atomicAdd(p.cand_count + 1, 1u);
       LB_ASSERT(c < (uint64_t)p.nsb * p.bl * p.k);
       p.clist[c] = (key << 22) | (uint64_t)(i - p.i0);
-      const uint32_t h = cbit(p, key);
+      const uint32_t h = cbit(p, jl, g);
       atomicOr(p.cb + (h >> 5), 1u << (h & 31));
     } else {
       arr |= 1ull << t;                  // first arrival
@@ -305,11 +306,11 @@ __global__ void __launch_bounds__(BL_THREADS) k5_resolve(const BloomParams p) {
     for (uint32_t t = 0; t < p.k; t++) {
       const uint64_t g = gen.next();
       if ((arr >> t) & 1) {
-        const uint64_t key = qkey(jl, g);
-        const uint32_t h = cbit(p, key);
+        const uint32_t h = cbit(p, jl, g);
         if (!((__ldg(p.cb + (h >> 5)) >> (h & 31)) & 1u)) {
           maybe = false;                                   // sole prober
         } else {                                           // (possibly) contested: join E
+          const uint64_t key = qkey(jl, g);
           if (np == 0) pk0 = key;
           else if (np == 1) pk1 = key;
           else e_add(p, key, i);
