@@ -35,6 +35,7 @@ thread_local std::string g_create_error;
 
 constexpr uint32_t kDefaultSubBatch = 32768;
 constexpr uint64_t kChunkTokens = 16ull << 20;   // host-batch staging chunk (64 MB of tokens)
+constexpr uint32_t K1_THREADS_HOST = 256;          // K1 block size (lb_minhash.cu), for chunk sizing
 constexpr uint64_t kGenMax = (1ull << 22) - 1;
 
 // Counter-mode expansion R(seed, dom, i) (DESIGN R5).
@@ -315,13 +316,19 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
   int c = 0;
   stage_begin(h, 0, s);
   while (d0 < n) {
-    // largest d1 with tokens [off[d0], off[d1]) <= chunk (at least one document)
+    // largest d1 with tokens [off[d0], off[d1]) <= chunk, but at least ~16 documents per
+    // resident K1 warp (long documents) and at least one document; buffers grow to fit
     const uint64_t t0 = b->offsets[d0];
     const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk);
     uint64_t d1 = (uint64_t)(lim - b->offsets) - 1;
+    d1 = std::max<uint64_t>(d1, std::min<uint64_t>(n, d0 + 16ull * h->sm_count * 2 * (K1_THREADS_HOST / 32)));
     if (d1 <= d0) d1 = d0 + 1;
     const uint64_t t1 = b->offsets[d1];
     const int buf = c & 1;
+    if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // a chunk larger than the buffer
+      LB_CUDA(h, cudaStreamSynchronize(s));
+      LB_CUDA(h, ensure(h->tok[buf], (t1 - t0) * sizeof(uint32_t)));
+    }
     LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
     LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
                                cudaMemcpyHostToDevice, h->copy_stream));
@@ -508,12 +515,17 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       const uint64_t t0 = b->offsets[d0];
       const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
       d1 = (uint64_t)(lim - b->offsets) - 1;
+      // at least ~16 documents per resident K1 warp, however long the documents: with full-text
+      // lengths 64 MB is ~1.7 documents per warp and a chunk would last as long as its slowest
+      // warp (C3 e2e: 155 vs 66 ms per 100K documents); the staging buffers grow to fit
+      const uint64_t min_docs = 16ull * h->sm_count * 2 * (K1_THREADS_HOST / 32);
+      d1 = std::max(d1, std::min(n, d0 + min_docs));
       if (d1 <= d0) d1 = d0 + 1;
       d1 = std::min(d1, fuse_chunk_end(d0, n));
       const uint64_t t1 = b->offsets[d1];
       if (t1 < t0) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease near index " + std::to_string(d0));
       const int buf = c & 1;
-      if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // one document larger than a chunk
+      if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // a chunk larger than the buffer
         LB_CUDA(h, cudaStreamSynchronize(s));
         LB_CUDA(h, ensure(h->tok[buf], (t1 - t0) * sizeof(uint32_t)));
       }
