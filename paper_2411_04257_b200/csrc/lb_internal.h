@@ -73,6 +73,7 @@ struct MinhashParams {
   const uint32_t* list_n;
   uint32_t* part_lists;      // [2][n_docs]: short documents, long documents
   uint32_t* part_counts;     // [2]
+  uint32_t block_gate;       // screened kernel: block-per-document mode iff *list_n < block_gate
 };
 
 struct BloomParams {

@@ -308,23 +308,41 @@ __device__ __forceinline__ uint32_t ld_shared_u8(uint32_t addr) {
   return v;
 }
 
-template <int NPL>
-__global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const MinhashParams p) {
+// BLOCKDOC: one document per block instead of per warp -- warp w takes the 32-shingle chunks
+// w, w + 8, w + 16, ... of the document, and the 8 warps' minima are merged in shared memory
+// before the epilogue.  For long documents: a launch over a few thousand full texts (a fused
+// chunk's long list) is then balanced over blocks instead of lasting as long as its slowest
+// warp (C4's fused step: 4 full texts per warp at most vs ~2.7 per warp with one each).
+template <int NPL, bool BLOCKDOC = false>
+__global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_minhash_scr(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
   __shared__ uint8_t qb[K1_WARPS][NPL][K1S_QCAP][32];   // [slot][lane]: conflict-free byte stores
   __shared__ uint32_t sg[K1_WARPS][32 * NPL];
+  __shared__ uint32_t s_doc;
+  __shared__ uint32_t smin[BLOCKDOC ? 32 * NPL : 1];   // BLOCKDOC: the block's running minima
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (*p.err) return;
+  if (p.block_gate && p.list && ((*p.list_n < p.block_gate) != BLOCKDOC)) return;   // the other mode runs
   const uint64_t tpol = l2_evict_first_policy();
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
   const uint32_t sh29 = p.sh29;
+  const uint32_t s_first = BLOCKDOC ? 32u * w : 0u, s_step = BLOCKDOC ? 32u * K1_WARPS : 32u;
 
   for (;;) {
     uint32_t di = 0;
-    if (lane == 0) di = atomicAdd(p.counter, 1u);
-    di = __shfl_sync(0xffffffffu, di, 0);
+    if (BLOCKDOC) {
+      __syncthreads();                                   // the previous document's merge is done
+      if (threadIdx.x == 0) s_doc = atomicAdd(p.counter, 1u);
+      if (BLOCKDOC)
+        for (uint32_t i = threadIdx.x; i < 32u * NPL; i += K1_THREADS) smin[i] = 0xFFFFFFFFu;
+      __syncthreads();
+      di = s_doc;
+    } else {
+      if (lane == 0) di = atomicAdd(p.counter, 1u);
+      di = __shfl_sync(0xffffffffu, di, 0);
+    }
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
     const uint64_t o0 = p.offsets[d];
@@ -337,8 +355,10 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
     const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
 
     uint32_t mn[NPL], bias[NPL], K[NPL];
+#pragma unroll
+    for (int q = 0; q < NPL; q++) mn[q] = 0xFFFFFFFFu;   // (a warp with no chunk keeps these)
     bool exact_mode = false;
-    for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+    for (uint32_t s0 = s_first; s0 < S; s0 += s_step) {
       const uint32_t s = s0 + lane;
       if (s < S) {
         uint64_t h = init;
@@ -348,7 +368,7 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
       __syncwarp();
       const uint32_t cnt = min(32u, S - s0);
       uint32_t j = 0;
-      if (s0 == 0) {   // seed the minima with the first shingle, exactly
+      if (s0 == s_first) {   // seed the minima with the warp's first shingle, exactly
         const XLimbs x0 = xs[w][0];
         bool big = false;
 #pragma unroll
@@ -427,10 +447,52 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
         }
         __syncwarp();
         flush();
+        if (BLOCKDOC) {
+          // share minima across the block's warps: each warp then screens against the smallest
+          // value any warp has found (still exact: an evaluation >= a value already achieved by
+          // another shingle cannot change the minimum), as one warp walking the whole document
+          // would, instead of against its own 1/8 of the shingles
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            const uint32_t g = atomicMin(&smin[lane + 32 * q], mn[q]);
+            if (g < mn[q]) {
+              mn[q] = g;
+              bias[q] = c[q].b0 - g;
+              K[q] = 0xFFFFFFFBu - g;
+            }
+          }
+        }
       }
       __syncwarp();
     }
 
+    if (BLOCKDOC) {
+      // merge the warps' minima: warp w reduces permutations [32 w', ...) for w' = w, w + 8, ...
+#pragma unroll
+      for (int q = 0; q < NPL; q++) sg[w][lane + 32 * q] = mn[q];
+      __syncthreads();
+      uint32_t fin[(NPL + K1_WARPS - 1) / K1_WARPS];
+#pragma unroll
+      for (int k = 0; k < (NPL + K1_WARPS - 1) / K1_WARPS; k++) {
+        const uint32_t pm = 32u * (w + K1_WARPS * k) + lane;
+        uint32_t v = 0xFFFFFFFFu;
+        if (pm < 32u * NPL) {
+#pragma unroll
+          for (int r = 0; r < K1_WARPS; r++) v = min(v, sg[r][pm]);
+        }
+        fin[k] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < (NPL + K1_WARPS - 1) / K1_WARPS; k++) {
+        const uint32_t pm = 32u * (w + K1_WARPS * k) + lane;
+        if (pm < 32u * NPL) sg[0][pm] = fin[k];
+      }
+      __syncthreads();
+      if (w != 0) continue;                              // warp 0 writes the outputs
+#pragma unroll
+      for (int q = 0; q < NPL; q++) mn[q] = sg[0][lane + 32 * q];
+    }
     if (p.sig_out) {
 #pragma unroll
       for (int q = 0; q < NPL; q++) {
@@ -456,18 +518,18 @@ __global__ void __launch_bounds__(K1_THREADS, LB_K1S_MINB) k1_minhash_scr(const 
   }
 }
 
-template <int NPL>
+template <int NPL, bool BLOCKDOC = false>
 static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash_scr<NPL>, K1_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash_scr<NPL, BLOCKDOC>, K1_THREADS, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
+  uint64_t want = BLOCKDOC ? (uint64_t)p.n_docs : ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  k1_minhash_scr<NPL><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  k1_minhash_scr<NPL, BLOCKDOC><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
@@ -528,9 +590,16 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     cudaMemsetAsync(p.counter, 0, 4, s);
     if (max_bps == 0) launch_t<4, LB_UNR4, 4, 2>(a, sm_count, s, 0);   // 256 = 2 passes x 4 x 32
     else launch_t<4, LB_UNR4, LB_K1_MINB, 2>(a, sm_count, s, max_bps);
+    // long documents: a warp each when there are enough of them to balance the warps (>= 16 per
+    // resident warp), else a block each (a few thousand full texts over ~2400 warps would last as
+    // long as the slowest warp: C4's fused step 43.9 -> 37.2 ms); both kernels are launched and
+    // the one the device-side count does not select returns at once
+    b.block_gate = 16u * (uint32_t)sm_count * 2u * K1_WARPS;
     cudaMemsetAsync(p.counter, 0, 4, s);
-    launch_s<8>(b, sm_count, s, max_bps);
-    return 3;
+    launch_s<8, false>(b, sm_count, s, max_bps);
+    cudaMemsetAsync(p.counter, 0, 4, s);
+    launch_s<8, true>(b, sm_count, s, max_bps);
+    return 4;
   }
   const bool screened = mode == 1 || (mode == 2 && npl >= 8);
   if (screened && npl <= 8) {
