@@ -19,7 +19,8 @@ def test_parity_cases_under_device_asserts():
     from paper_2411_04257_b200 import build
     build.build(checked=True)
     env = dict(os.environ, LSHBLOOM_LIB=build.LIB_CHECKED)
-    sel = "dense or edge or sub_batch or shapes or single_document or malformed or many_chunks or both_minhash"
+    sel = ("dense or edge or sub_batch or shapes or single_document or malformed or many_chunks or both_minhash"
+           " or partition")
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-k", sel,
                           os.path.join(ROOT, "tests", "test_gpu_parity.py")],
                          env=env, cwd=ROOT, capture_output=True, text=True, timeout=1500)
