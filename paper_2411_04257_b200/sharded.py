@@ -69,7 +69,10 @@ class ShardedLSHBloom:
         counts = self._counts(n_local, device)
         if self.exchange == "p2p":
             return self._query_insert_p2p(offsets, tokens, counts, device)
-        send = self.engine.band_hashes_sharded(offsets, tokens)          # owner-major, flat
+        if n_local:
+            send = self.engine.band_hashes_sharded(offsets, tokens)      # owner-major, flat
+        else:                                                            # this rank has no documents
+            send = torch.empty(0, dtype=torch.int64, device=device)
         in_splits = [n_local * w for w in self.widths]
         out_splits = [c * self.bl for c in counts]
         recv = torch.empty(sum(out_splits), dtype=send.dtype, device=device)

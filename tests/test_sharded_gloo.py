@@ -73,9 +73,12 @@ def _worker(rank, world, port, cuts, n_total, out_path):
 def test_sharded_flags_equal_single_process_oracle(world, tmp_path):
     # two stream batches; each split into `world` unequal contiguous rank shards
     rng = np.random.default_rng(world)
-    bounds = [0, 1400, 3000]
+    bounds = [0, 1400, 1401, 3000]                       # includes a one-document batch
     cuts = []
     for a, b in zip(bounds[:-1], bounds[1:]):
+        if b - a < world:                                 # fewer documents than ranks: empty shards
+            cuts.append([a] * world + [b])
+            continue
         inner = sorted(rng.choice(np.arange(a + 1, b), world - 1, replace=False).tolist())
         cuts.append([a] + inner + [b])
     out = str(tmp_path / "flags_%d.npy")
