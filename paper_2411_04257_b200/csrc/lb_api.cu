@@ -50,7 +50,9 @@ struct lshbloom {
   uint32_t k = 0, band_lo = 0, band_hi = 0, bl = 0, npl = 0, sub_batch = 0;
   int device = 0, sm_count = 148;
   cudaStream_t own_stream = nullptr, copy_stream = nullptr, bloom_stream = nullptr;
-  cudaEvent_t ev_fuse = nullptr;
+  cudaStream_t k1_stream2 = nullptr;  // fused step: odd K1 chunks, so a chunk's tail overlaps the next
+  cudaEvent_t ev_fuse = nullptr, ev_join = nullptr;
+  bool k1_alt = true;
   int k1_bps = 0;                 // K1 blocks per SM cap (0 = occupancy limit)
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_k1[2] = {nullptr, nullptr};
   PermCoef* d_coef = nullptr;
@@ -142,6 +144,8 @@ void free_all(lshbloom* h) {
   for (int i = 0; i < 4; i++)
     if (h->tev[i]) cudaEventDestroy(h->tev[i]);
   if (h->ev_fuse) cudaEventDestroy(h->ev_fuse);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->k1_stream2) cudaStreamDestroy(h->k1_stream2);
   if (h->bloom_stream) cudaStreamDestroy(h->bloom_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -473,11 +477,8 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   const uint64_t n = b->n_docs;
   uint64_t* bh = (uint64_t*)h->bh.p;
   MinhashParams p = base_params(h);
-  if (h->npl >= 8) {   // scratch of the length-partitioned K1 launches (lb_minhash.cu)
-    LB_CUDA(h, ensure(h->part, (2 * (size_t)b->n_docs + 2) * sizeof(uint32_t)));
-    p.part_lists = (uint32_t*)h->part.p;
-    p.part_counts = (uint32_t*)h->part.p + 2 * b->n_docs;
-  }
+  if (h->npl >= 8)   // scratch of the length-partitioned K1 launches (lb_minhash.cu), per K1 stream
+    LB_CUDA(h, ensure(h->part, (4 * (size_t)b->n_docs + 4) * sizeof(uint32_t)));
   p.bh_out = bh;
   p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
   int rc = reset_err(h, s);
@@ -503,7 +504,12 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, s));
   LB_CUDA(h, cudaEventRecord(h->ev_fuse, s));
   LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
-  p.counter = h->d_counters + 1;
+  // K1 chunks alternate between s and k1_stream2: each launch ends with a tail in which its last
+  // documents finish on a few warps, and the next chunk's blocks fill the SM slots meanwhile.
+  // Each stream has its own work counter, partition scratch and staging buffer (host batches).
+  const bool alt = h->k1_alt;
+  cudaStream_t kst[2] = {s, alt ? h->k1_stream2 : s};
+  if (alt) LB_CUDA(h, cudaStreamWaitEvent(h->k1_stream2, h->ev_fuse, 0));
   uint64_t d0 = 0;
   int c = 0;
   stage_begin(h, 0, s);
@@ -526,27 +532,40 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       if (t1 < t0) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease near index " + std::to_string(d0));
       const int buf = c & 1;
       if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // a chunk larger than the buffer
-        LB_CUDA(h, cudaStreamSynchronize(s));
+        LB_CUDA(h, cudaStreamSynchronize(kst[buf]));
         LB_CUDA(h, ensure(h->tok[buf], (t1 - t0) * sizeof(uint32_t)));
       }
       LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
       LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, h->copy_stream));
       LB_CUDA(h, cudaEventRecord(h->ev_h2d[buf], h->copy_stream));
-      LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_h2d[buf], 0));
+      LB_CUDA(h, cudaStreamWaitEvent(kst[buf], h->ev_h2d[buf], 0));
       p.tokens = (const uint32_t*)h->tok[buf].p;
       p.tok_base = t0;
     }
+    const int par = c & 1;
+    cudaStream_t ks = kst[par];
     p.doc0 = (uint32_t)d0;
     p.n_docs = (uint32_t)(d1 - d0);
-    LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, s));
-    int l = launch_minhash(p, (int)h->npl, h->sm_count, s, h->k1_bps);
+    p.counter = h->d_counters + 1 + par;
+    if (h->npl >= 8) {
+      p.part_lists = (uint32_t*)h->part.p + (size_t)par * 2 * n;
+      p.part_counts = (uint32_t*)h->part.p + 4 * n + 2 * par;
+    }
+    LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, ks));
+    int l = launch_minhash(p, (int)h->npl, h->sm_count, ks, h->k1_bps);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     h->launches += l;
     LB_CUDA(h, cudaGetLastError());
-    if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[c & 1], s));
-    if (d1 == n) stage_end(h, 0, s);
-    LB_CUDA(h, cudaEventRecord(h->ev_fuse, s));
+    if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[par], ks));
+    LB_CUDA(h, cudaEventRecord(h->ev_fuse, ks));
+    if (d1 == n) {   // both K1 streams joined into s before the stage's end mark
+      if (alt) {
+        LB_CUDA(h, cudaEventRecord(h->ev_join, h->k1_stream2));
+        LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_join, 0));
+      }
+      stage_end(h, 0, s);
+    }
     LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
     if ((rc = run_bloom(h, bh, n, 1, d0, d1, ddup, h->bloom_stream, d0 == 0, d1 == n))) return rc;
     d0 = d1;
@@ -661,6 +680,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     CR(cudaStreamCreateWithPriority(&h->bloom_stream, cudaStreamNonBlocking, hi));
   }
   CR(cudaEventCreateWithFlags(&h->ev_fuse, cudaEventDisableTiming));
+  CR(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  CR(cudaStreamCreateWithFlags(&h->k1_stream2, cudaStreamNonBlocking));
+  if (const char* e = getenv("LSHBLOOM_K1_ALT")) h->k1_alt = atoi(e) != 0;
   h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
   if (const char* e = getenv("LSHBLOOM_K1_BPS")) h->k1_bps = atoi(e);
   for (int i = 0; i < 2; i++) {
