@@ -449,23 +449,31 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
   return LSHBLOOM_OK;
 }
 
-// query_insert: K1 over document chunks on the caller's stream s, each chunk's Bloom
-// sub-batches on bloom_stream as soon as its band hashes exist, so the integer-bound K1 of
-// chunk c+1 overlaps the memory-bound Bloom kernels of chunk c.  Bloom sub-batches stay in
-// document order (one stream), which is all the exact semantics need.
-constexpr uint64_t kFuseEdgeDocs = 32768;   // small first / last chunks: Bloom starts early, short tail
+// query_insert: K1 over document chunks (alternately on the caller's stream s and k1_stream2),
+// each chunk's Bloom sub-batches on bloom_stream as soon as its band hashes exist, so the
+// integer-bound K1 of chunk c+1 overlaps the memory-bound Bloom kernels of chunk c.  Bloom
+// sub-batches stay in document order (one stream), which is all the exact semantics need.
+uint64_t fuse_edge_docs() {   // small first / last chunks: Bloom starts early, short tail
+  static uint64_t v = 0;
+  if (!v) {
+    const char* e = getenv("LSHBLOOM_FUSE_EDGE");
+    v = e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 16384;
+  }
+  return v;
+}
 
 uint64_t fuse_docs() {
   static uint64_t v = 0;
   if (!v) {
     const char* e = getenv("LSHBLOOM_FUSE_DOCS");
-    v = e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 131072;
+    v = e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 32768;
   }
   return v;
 }
 
 uint64_t fuse_chunk_end(uint64_t d0, uint64_t n) {
   const uint64_t kFuseDocs = fuse_docs();
+  const uint64_t kFuseEdgeDocs = fuse_edge_docs();
   if (d0 == 0) return std::min(n, kFuseEdgeDocs);
   const uint64_t left = n - d0;
   if (left <= kFuseEdgeDocs) return n;
