@@ -275,7 +275,7 @@ def test_sharded_layer_world1_nccl(c1):
 
 @pytest.mark.parametrize("on_device", [True, False])
 def test_many_chunks_short_docs(on_device):
-    # > 2 fused K1/Bloom chunks (131072 docs each) and, on the host path, > 1 staging chunk
+    # many fused K1/Bloom chunks (alternating K1 streams) and, on the host path, > 1 staging chunk
     from synthetic.corpus import CorpusConfig, LengthDist
     cfg = CorpusConfig("short", 300_000, LengthDist(60, 30), 5000, 1.1, 0.1, "edit", 0.0, 0.1,
                        num_perm=64, b=8, r=8, fp_rate=1e-4)
@@ -342,4 +342,39 @@ print("ok")
     env = dict(os.environ, LSHBLOOM_K1_SPLIT_S=split, PYTHONPATH=root)
     env.pop("LSHBLOOM_K1", None)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"LSHBLOOM_K1_ALT": "0"},
+                                 {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_FUSE_EDGE": "1024"},
+                                 {"LSHBLOOM_FUSE_DOCS": "1500", "LSHBLOOM_FUSE_EDGE": "1100", "LSHBLOOM_K1_ALT": "1"}])
+def test_fused_chunking_knobs(env):
+    # the fused step's K1 chunking (one or two K1 streams, chunk sizes) changes only the schedule:
+    # flags equal the oracle's with 128 and 256 permutations (the latter with the length-split
+    # K1 and its per-stream partition scratch), device and host inputs, many chunks per call
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, oracle
+from synthetic.corpus import CONFIGS, gen_range
+from paper_2411_04257_b200 import LSHBloom
+for name, n, P, b, r in (("C1", 9000, 128, 16, 8), ("C4", 7000, 256, 32, 8)):
+    cfg = CONFIGS[name]
+    off, tok = gen_range(cfg, 0, n)
+    _, bh, dup, _ = oracle.run(off, tok, num_perm=P, b=b, r=r, n_expected=n, fp_rate=1e-4, seed=5)
+    assert 0 < dup.sum() < n
+    d = (torch.from_numpy(off.view(np.int64)).cuda(), torch.from_numpy(tok.view(np.int32)).cuda())
+    for args in (d, (off, tok)):
+        idx = LSHBloom(P, b, r, n, 1e-4, 5, device=0)
+        got = idx.query_insert(*args)
+        got = got.cpu().numpy() if hasattr(got, "cpu") else np.asarray(got)
+        assert (got == dup).all(), (name, np.flatnonzero(got != dup)[:10])
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    full = dict(os.environ, PYTHONPATH=root, **env)
+    for k in ("LSHBLOOM_K1", "LSHBLOOM_K1_SPLIT_S"):
+        full.pop(k, None)
+    out = subprocess.run([sys.executable, "-c", code], env=full, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
