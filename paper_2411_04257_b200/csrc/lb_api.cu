@@ -529,10 +529,18 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       const uint64_t t0 = b->offsets[d0];
       const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
       d1 = (uint64_t)(lim - b->offsets) - 1;
-      // at least ~16 documents per resident K1 warp, however long the documents: with full-text
-      // lengths 64 MB is ~1.7 documents per warp and a chunk would last as long as its slowest
-      // warp (C3 e2e: 155 vs 66 ms per 100K documents); the staging buffers grow to fit
-      const uint64_t min_docs = 16ull * h->sm_count * 2 * (K1_THREADS_HOST / 32);
+      // at least ~3.5 documents per resident K1 warp (8192 on 148 SMs), however long the
+      // documents: with full-text lengths 64 MB is ~1.7 documents per warp and a chunk would last
+      // as long as its slowest warp (C3 e2e: 155 vs 66 ms per 100K documents).  With the two K1
+      // streams the next chunk fills that tail, so the floor is lower than with one stream (16
+      // per warp): C3 e2e 71.8 -> 70.0 ms per 100K, C4 36.5 -> 35.7 ms per 200K (2K-16K swept).
+      // The staging buffers grow to fit.
+      static const uint64_t env_min_docs = [] {
+        const char* e = getenv("LSHBLOOM_HOST_MIN_DOCS");
+        return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) : 0;
+      }();
+      const uint64_t min_docs =
+          env_min_docs ? env_min_docs : (7ull * h->sm_count * 2 * (K1_THREADS_HOST / 32) + 1) / 2;
       d1 = std::max(d1, std::min(n, d0 + min_docs));
       if (d1 <= d0) d1 = d0 + 1;
       d1 = std::min(d1, fuse_chunk_end(d0, n));
