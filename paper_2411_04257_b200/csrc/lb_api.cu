@@ -54,7 +54,7 @@ struct lshbloom {
   cudaEvent_t ev_fuse = nullptr, ev_join = nullptr;
   bool k1_alt = true;
   int k1_bps = 0;                 // K1 blocks per SM cap (0 = occupancy limit)
-  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_k1[2] = {nullptr, nullptr};
+  cudaEvent_t ev_h2d[3] = {nullptr, nullptr, nullptr}, ev_k1[3] = {nullptr, nullptr, nullptr};
   PermCoef* d_coef = nullptr;
   uint64_t* d_bcoef = nullptr;
   uint64_t* d_s1 = nullptr;
@@ -73,7 +73,7 @@ struct lshbloom {
   uint32_t* d_cb = nullptr;       // contested-position summary bits (2^cb_log2)
   uint32_t cb_log2 = 26;            // 8 MB: ~0.2 % of first arrivals collide with a contested position
   ErrState* d_err = nullptr;
-  DevBuf off, tok[2], bh, dup, sig, part;
+  DevBuf off, tok[3], bh, dup, sig, part;   // tok: host-batch staging buffers
   uint64_t doc_count = 0, launches = 0;
   // classic MinHashLSH index (index_kind = LSHBLOOM_INDEX_CLASSIC)
   uint64_t* d_ckeys = nullptr;    // [bl][2^c_log2cap]
@@ -136,8 +136,8 @@ void free_all(lshbloom* h) {
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_clist); F(h->d_cb); F(h->d_ekey);
   F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
-  F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
-  for (int i = 0; i < 2; i++) {
+  F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->tok[2].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
+  for (int i = 0; i < 3; i++) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
   }
@@ -453,6 +453,20 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
 // each chunk's Bloom sub-batches on bloom_stream as soon as its band hashes exist, so the
 // integer-bound K1 of chunk c+1 overlaps the memory-bound Bloom kernels of chunk c.  Bloom
 // sub-batches stay in document order (one stream), which is all the exact semantics need.
+// Staging buffers of a host batch in the fused step.  A third buffer lets the copy of chunk
+// c+3 start when K1 of chunk c ends instead of c+1's: with long documents (large chunks) that
+// keeps the copy ahead (C3 e2e 70.8 -> 67.5 ms per 100K, C4 35.8 -> 33.8 ms per 200K); with
+// abstract lengths it costs a little (C2 19.64 -> 19.72 ms), so: 3 when the batch averages
+// more than 512 tokens per document.  LSHBLOOM_HOST_BUFS=2|3 overrides.
+int host_bufs(uint64_t n_docs, uint64_t n_tokens) {
+  static const int v = [] {
+    const char* e = getenv("LSHBLOOM_HOST_BUFS");
+    return e ? (atoi(e) == 3 ? 3 : 2) : 0;
+  }();
+  if (v) return v;
+  return n_tokens > 512 * n_docs ? 3 : 2;
+}
+
 uint64_t fuse_edge_docs() {   // small first / last chunks: Bloom starts early, short tail
   static uint64_t v = 0;
   if (!v) {
@@ -492,6 +506,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   int rc = reset_err(h, s);
   if (rc) return rc;
   uint64_t chunk_tokens = 0;
+  int nbuf = 2;
   if (b->on_device) {
     h->launches += launch_validate(b->offsets, n, h->d_err, s);
     p.offsets = b->offsets;
@@ -505,8 +520,9 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     LB_CUDA(h, cudaMemcpyAsync(h->off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     h->launches += launch_validate((const uint64_t*)h->off.p, n, h->d_err, s);
     chunk_tokens = kChunkTokens;
+    nbuf = host_bufs(n, b->offsets[n]);
     const uint64_t buf_tokens = std::max<uint64_t>(1, std::min(chunk_tokens, b->offsets[n]));
-    for (int i = 0; i < 2; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
+    for (int i = 0; i < nbuf; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
     p.offsets = (const uint64_t*)h->off.p;
   }
   LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, s));
@@ -546,16 +562,16 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       d1 = std::min(d1, fuse_chunk_end(d0, n));
       const uint64_t t1 = b->offsets[d1];
       if (t1 < t0) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease near index " + std::to_string(d0));
-      const int buf = c & 1;
+      const int buf = c % nbuf;
       if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // a chunk larger than the buffer
-        LB_CUDA(h, cudaStreamSynchronize(kst[buf]));
+        LB_CUDA(h, cudaEventSynchronize(h->ev_k1[buf]));   // its last reader is done
         LB_CUDA(h, ensure(h->tok[buf], (t1 - t0) * sizeof(uint32_t)));
       }
       LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_k1[buf], 0));
       LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, h->copy_stream));
       LB_CUDA(h, cudaEventRecord(h->ev_h2d[buf], h->copy_stream));
-      LB_CUDA(h, cudaStreamWaitEvent(kst[buf], h->ev_h2d[buf], 0));
+      LB_CUDA(h, cudaStreamWaitEvent(kst[c & 1], h->ev_h2d[buf], 0));
       p.tokens = (const uint32_t*)h->tok[buf].p;
       p.tok_base = t0;
     }
@@ -573,7 +589,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     h->launches += l;
     LB_CUDA(h, cudaGetLastError());
-    if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[par], ks));
+    if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[c % nbuf], ks));
     LB_CUDA(h, cudaEventRecord(h->ev_fuse, ks));
     if (d1 == n) {   // both K1 streams joined into s before the stage's end mark
       if (alt) {
@@ -701,7 +717,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   if (const char* e = getenv("LSHBLOOM_K1_ALT")) h->k1_alt = atoi(e) != 0;
   h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
   if (const char* e = getenv("LSHBLOOM_K1_BPS")) h->k1_bps = atoi(e);
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < 3; i++) {
     CR(cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming));
     CR(cudaEventCreateWithFlags(&h->ev_k1[i], cudaEventDisableTiming));
     CR(cudaEventRecord(h->ev_k1[i], h->own_stream));
