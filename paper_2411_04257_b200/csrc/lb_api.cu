@@ -476,17 +476,19 @@ uint64_t fuse_edge_docs() {   // small first / last chunks: Bloom starts early, 
   return v;
 }
 
-uint64_t fuse_docs() {
-  static uint64_t v = 0;
-  if (!v) {
+// Middle K1 chunk, swept per workload with the two K1 streams: 128 permutations (C2) 32K
+// documents (16K: 19.16 vs 18.98 ms); 256 (the length-split K1 of C3 / C4) 16K (C4 32.3 vs
+// 34.2 ms per 200K, C3 63.3 vs 64.5 ms per 100K; 8K and 12K slower).
+uint64_t fuse_docs(uint32_t npl) {
+  static const uint64_t v = [] {
     const char* e = getenv("LSHBLOOM_FUSE_DOCS");
-    v = e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 32768;
-  }
-  return v;
+    return e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : 0;
+  }();
+  return v ? v : (npl >= 8 ? 16384 : 32768);
 }
 
-uint64_t fuse_chunk_end(uint64_t d0, uint64_t n) {
-  const uint64_t kFuseDocs = fuse_docs();
+uint64_t fuse_chunk_end(uint64_t d0, uint64_t n, uint32_t npl) {
+  const uint64_t kFuseDocs = fuse_docs(npl);
   const uint64_t kFuseEdgeDocs = fuse_edge_docs();
   if (d0 == 0) return std::min(n, kFuseEdgeDocs);
   const uint64_t left = n - d0;
@@ -540,7 +542,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   while (d0 < n) {
     uint64_t d1;
     if (b->on_device) {
-      d1 = fuse_chunk_end(d0, n);
+      d1 = fuse_chunk_end(d0, n, h->npl);
     } else {
       const uint64_t t0 = b->offsets[d0];
       const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
@@ -559,7 +561,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
           env_min_docs ? env_min_docs : (7ull * h->sm_count * 2 * (K1_THREADS_HOST / 32) + 1) / 2;
       d1 = std::max(d1, std::min(n, d0 + min_docs));
       if (d1 <= d0) d1 = d0 + 1;
-      d1 = std::min(d1, fuse_chunk_end(d0, n));
+      d1 = std::min(d1, fuse_chunk_end(d0, n, h->npl));
       const uint64_t t1 = b->offsets[d1];
       if (t1 < t0) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease near index " + std::to_string(d0));
       const int buf = c % nbuf;
