@@ -50,8 +50,9 @@ struct lshbloom {
   uint32_t k = 0, band_lo = 0, band_hi = 0, bl = 0, npl = 0, sub_batch = 0;
   int device = 0, sm_count = 148;
   cudaStream_t own_stream = nullptr, copy_stream = nullptr, bloom_stream = nullptr;
-  cudaStream_t k1_stream2 = nullptr;  // fused step: odd K1 chunks, so a chunk's tail overlaps the next
-  cudaEvent_t ev_fuse = nullptr, ev_join = nullptr;
+  cudaStream_t k1_stream2 = nullptr, k1_stream3 = nullptr;  // fused step: K1 chunks round-robin, a chunk's tail overlaps the next
+  cudaEvent_t ev_fuse = nullptr, ev_join = nullptr, ev_join3 = nullptr;
+  int k1_nstreams = 2;
   bool k1_alt = true;
   int k1_bps = 0;                 // K1 blocks per SM cap (0 = occupancy limit)
   cudaEvent_t ev_h2d[3] = {nullptr, nullptr, nullptr}, ev_k1[3] = {nullptr, nullptr, nullptr};
@@ -68,7 +69,7 @@ struct lshbloom {
   uint64_t gen = 1;
   uint64_t* d_st = nullptr;       // 2 * sub_batch * bl
   uint32_t* d_cand = nullptr;     // sub_batch * bl
-  uint32_t* d_counters = nullptr; // [1..2] K1 work counters, [8] classic full, [12..13] Bloom candidates / contested
+  uint32_t* d_counters = nullptr; // [1..3] K1 work counters, [8] classic full, [12..13] Bloom candidates / contested
   uint64_t* d_clist = nullptr;    // contested probes of a sub-batch (sub_batch * bl * k)
   uint32_t* d_cb = nullptr;       // contested-position summary bits (2^cb_log2)
   uint32_t cb_log2 = 26;            // 8 MB: ~0.2 % of first arrivals collide with a contested position
@@ -146,6 +147,8 @@ void free_all(lshbloom* h) {
   if (h->ev_fuse) cudaEventDestroy(h->ev_fuse);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->k1_stream2) cudaStreamDestroy(h->k1_stream2);
+  if (h->k1_stream3) cudaStreamDestroy(h->k1_stream3);
+  if (h->ev_join3) cudaEventDestroy(h->ev_join3);
   if (h->bloom_stream) cudaStreamDestroy(h->bloom_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -502,7 +505,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   uint64_t* bh = (uint64_t*)h->bh.p;
   MinhashParams p = base_params(h);
   if (h->npl >= 8)   // scratch of the length-partitioned K1 launches (lb_minhash.cu), per K1 stream
-    LB_CUDA(h, ensure(h->part, (4 * (size_t)b->n_docs + 4) * sizeof(uint32_t)));
+    LB_CUDA(h, ensure(h->part, (6 * (size_t)b->n_docs + 6) * sizeof(uint32_t)));
   p.bh_out = bh;
   p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
   int rc = reset_err(h, s);
@@ -534,8 +537,9 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   // documents finish on a few warps, and the next chunk's blocks fill the SM slots meanwhile.
   // Each stream has its own work counter, partition scratch and staging buffer (host batches).
   const bool alt = h->k1_alt;
-  cudaStream_t kst[2] = {s, alt ? h->k1_stream2 : s};
-  if (alt) LB_CUDA(h, cudaStreamWaitEvent(h->k1_stream2, h->ev_fuse, 0));
+  const int nks = alt ? h->k1_nstreams : 1;
+  cudaStream_t kst[3] = {s, h->k1_stream2, h->k1_stream3};
+  for (int k = 1; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_fuse, 0));
   uint64_t d0 = 0;
   int c = 0;
   stage_begin(h, 0, s);
@@ -573,18 +577,18 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       LB_CUDA(h, cudaMemcpyAsync(h->tok[buf].p, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, h->copy_stream));
       LB_CUDA(h, cudaEventRecord(h->ev_h2d[buf], h->copy_stream));
-      LB_CUDA(h, cudaStreamWaitEvent(kst[c & 1], h->ev_h2d[buf], 0));
+      LB_CUDA(h, cudaStreamWaitEvent(kst[c % nks], h->ev_h2d[buf], 0));
       p.tokens = (const uint32_t*)h->tok[buf].p;
       p.tok_base = t0;
     }
-    const int par = c & 1;
+    const int par = c % nks;
     cudaStream_t ks = kst[par];
     p.doc0 = (uint32_t)d0;
     p.n_docs = (uint32_t)(d1 - d0);
     p.counter = h->d_counters + 1 + par;
     if (h->npl >= 8) {
       p.part_lists = (uint32_t*)h->part.p + (size_t)par * 2 * n;
-      p.part_counts = (uint32_t*)h->part.p + 4 * n + 2 * par;
+      p.part_counts = (uint32_t*)h->part.p + 6 * n + 2 * par;
     }
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, ks));
     int l = launch_minhash(p, (int)h->npl, h->sm_count, ks, h->k1_bps);
@@ -593,10 +597,11 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     LB_CUDA(h, cudaGetLastError());
     if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[c % nbuf], ks));
     LB_CUDA(h, cudaEventRecord(h->ev_fuse, ks));
-    if (d1 == n) {   // both K1 streams joined into s before the stage's end mark
-      if (alt) {
-        LB_CUDA(h, cudaEventRecord(h->ev_join, h->k1_stream2));
-        LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_join, 0));
+    if (d1 == n) {   // every K1 stream joined into s before the stage's end mark
+      cudaEvent_t ej[3] = {nullptr, h->ev_join, h->ev_join3};
+      for (int k = 1; k < nks; k++) {
+        LB_CUDA(h, cudaEventRecord(ej[k], kst[k]));
+        LB_CUDA(h, cudaStreamWaitEvent(s, ej[k], 0));
       }
       stage_end(h, 0, s);
     }
@@ -716,6 +721,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaEventCreateWithFlags(&h->ev_fuse, cudaEventDisableTiming));
   CR(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   CR(cudaStreamCreateWithFlags(&h->k1_stream2, cudaStreamNonBlocking));
+  CR(cudaStreamCreateWithFlags(&h->k1_stream3, cudaStreamNonBlocking));
+  CR(cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming));
+  if (const char* e = getenv("LSHBLOOM_K1_STREAMS")) h->k1_nstreams = std::min(3, std::max(1, atoi(e)));
   if (const char* e = getenv("LSHBLOOM_K1_ALT")) h->k1_alt = atoi(e) != 0;
   h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
   if (const char* e = getenv("LSHBLOOM_K1_BPS")) h->k1_bps = atoi(e);
