@@ -30,11 +30,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synthetic.corpus import CONFIGS, checksum, gen_range  # noqa: E402
+from synthetic.corpus import CONFIGS, checksum, gen_range, gen_range_parallel  # noqa: E402
 
 METRIC = "documents/sec end-to-end at 1/2/4/8 B200; % of INT-pipe and HBM roofline"
 UNIT = "docs/s"
-DOCS_PER_RANK = 1_000_000
+# documents per rank per step (one batch of the config's stream)
+DOCS_PER_STEP = {"C1": 10_000, "C2": 1_000_000, "C3": 200_000, "C4": 400_000, "C5": 4_000_000}
 
 
 def parse():
@@ -43,8 +44,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--docs", type=int, default=DOCS_PER_RANK, help="documents per rank per step")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--docs", type=int, default=0, help="documents per rank per step (default: per config)")
+    ap.add_argument("--n-expected", type=int, default=0,
+                    help="index capacity n (default: the config's corpus size, BASELINE.json)")
     ap.add_argument("--sub-batch", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -56,7 +59,12 @@ def parse():
                     help="N > 1: band-hash / flag exchange over peer memory (default) or NCCL")
     ap.add_argument("--hbm-docs", type=int, default=1_000_000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if not a.docs:
+        a.docs = DOCS_PER_STEP[a.config]
+    if not a.n_expected:
+        a.n_expected = CONFIGS[a.config].n_docs
+    return a
 
 
 def dist_env():
@@ -128,7 +136,7 @@ class ClockSampler:
 
 def workload(cfg, rank: int, n_docs: int):
     t = time.time()
-    off, tok = gen_range(cfg, rank * n_docs, (rank + 1) * n_docs)
+    off, tok = gen_range_parallel(cfg, rank * n_docs, (rank + 1) * n_docs)
     return off, tok, time.time() - t
 
 
@@ -185,12 +193,12 @@ def run_reference(args, cfg):
     off, tok, _ = workload(cfg, 0, args.docs)
     # each step: a bounded sample so (warmup + steps) finishes within a few minutes
     per_step = max(2.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
-    sample = calibrate_sample(cfg, off, tok, args.docs * max(1, args.gpus), nthreads, per_step)
+    sample = calibrate_sample(cfg, off, tok, args.n_expected, nthreads, per_step)
     for _ in range(args.warmup):
-        oracle_sample(cfg, off, tok, args.docs, sample, nthreads)
+        oracle_sample(cfg, off, tok, args.n_expected, sample, nthreads)
     t = 0.0
     for _ in range(args.steps):
-        t += oracle_sample(cfg, off, tok, args.docs, sample, nthreads)
+        t += oracle_sample(cfg, off, tok, args.n_expected, sample, nthreads)
     value = sample * args.steps / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -320,7 +328,7 @@ def main():
     evals = minhash_evals(off, cfg.num_perm, cfg.shingle_n)
 
     if world > 1:
-        sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, n_total, cfg.fp_rate, cfg.seed,
+        sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, args.n_expected, cfg.fp_rate, cfg.seed,
                              device=local, sub_batch=args.sub_batch, exchange=args.exchange, index=args.index)
         if args.exchange == "p2p":
             try:                              # symmetric-memory rendezvous; NCCL if unavailable
@@ -331,7 +339,7 @@ def main():
         eng = sx.engine
         step = lambda o, t: sx.query_insert(o, t)  # noqa: E731
     else:
-        eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n_total, cfg.fp_rate, cfg.seed, device=local,
+        eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, args.n_expected, cfg.fp_rate, cfg.seed, device=local,
                        sub_batch=args.sub_batch, index=args.index)
         sx = None
         d_flags = torch.empty(args.docs, dtype=torch.uint8, device=dev)   # caller-owned output (no allocation per step)
@@ -474,8 +482,8 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         nthreads = os.cpu_count() or 1
-        sample = calibrate_sample(cfg, off, tok, n_total, nthreads, args.cpu_seconds)
-        dt = oracle_sample(cfg, off, tok, n_total, sample, nthreads)
+        sample = calibrate_sample(cfg, off, tok, args.n_expected, nthreads, args.cpu_seconds)
+        dt = oracle_sample(cfg, off, tok, args.n_expected, sample, nthreads)
         cpu = {"value": sample / dt, "unit": UNIT, "cores": nthreads, "kind": "oracle",
                "sample": "first %d of %d docs of %s (signatures, band hashes, stream-order Bloom), %.1f s"
                          % (sample, args.docs, cfg.name, dt)}
@@ -490,7 +498,7 @@ def main():
                                                                     cfg.length.sd, cfg.zipf_s, cfg.vocab,
                                                                     int(cfg.dup_frac * 100), cfg.shingle_n),
                    "num_perm": cfg.num_perm, "b": cfg.b, "r": cfg.r, "fp_rate": cfg.fp_rate,
-                   "n_expected": n_total, "docs_per_step": n_total, "tokens_per_rank": int(len(tok)),
+                   "n_expected": args.n_expected, "docs_per_step": n_total, "tokens_per_rank": int(len(tok)),
                    "index": args.index, "index_bytes": int(eng.info()["filter_bytes"]),
                    "parallelism": ("band-sharded x%d, %s exchange" % (world, args.exchange)) if world > 1
                                   else "single GPU",

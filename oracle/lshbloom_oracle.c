@@ -37,10 +37,12 @@
  * exact-band-equality index; Bloom FP / fill against their
  * analytic values.
  *
- * Parity unpinned (documented conventions whose exact values nothing outside
- * this file fixes; pinned only by the properties listed in DESIGN.md §2):
- * orc_fingerprint (DESIGN R1) and orc_probes_blocked's in-block offsets (the
- * blocked variant, is this build's own definition).
+ * Conventions the paper leaves open (orc_fingerprint, DESIGN R1; orc_family,
+ * R5; orc_probes_blocked's in-block offsets) are pinned
+ * element by element against an independent pure-Python big-integer
+ * re-implementation written from DESIGN.md's prose (tests/support/
+ * micro_oracle.py, tests/test_oracle_micro.py) and by known-answer vectors
+ * (tests/golden/conventions_kat.json).
  */
 #include <math.h>
 #include <pthread.h>

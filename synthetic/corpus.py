@@ -255,6 +255,39 @@ def gen_range(cfg: CorpusConfig, start: int, stop: int, chunk: int = 65536):
     return np.concatenate(offs), (np.concatenate(toks) if toks else np.zeros(0, np.uint32))
 
 
+def _gen_chunk(args):
+    cfg, c0, c1 = args
+    return gen_docs(cfg, np.arange(c0, c1))
+
+
+def gen_range_parallel(cfg: CorpusConfig, start: int, stop: int, workers: int | None = None,
+                       chunk: int = 0):
+    """gen_range over a process pool (chunks are independent: every document is a pure function
+    of (corpus seed, index)).  Byte-identical to gen_range; used for the multi-GB C3-C5 batches."""
+    import multiprocessing as mp
+    import os
+    workers = workers or min(32, os.cpu_count() or 1)
+    chunk = chunk or max(2048, min(65536, (stop - start) // (4 * workers) + 1))
+    jobs = [(cfg, c0, min(stop, c0 + chunk)) for c0 in range(start, stop, chunk)]
+    if workers <= 1 or len(jobs) <= 1:
+        return gen_range(cfg, start, stop, chunk)
+    with mp.get_context("fork").Pool(min(workers, len(jobs))) as pool:
+        parts = pool.map(_gen_chunk, jobs, chunksize=1)
+    lens = [len(t) for _, t in parts]
+    total = int(sum(lens))
+    offsets = np.empty(stop - start + 1, np.uint64)
+    offsets[0] = 0
+    tokens = np.empty(total, np.uint32)
+    base, d = 0, 0
+    for o, t in parts:
+        n = len(o) - 1
+        offsets[d + 1:d + 1 + n] = o[1:] + np.uint64(base)
+        tokens[base:base + len(t)] = t
+        base += len(t)
+        d += n
+    return offsets, tokens
+
+
 def checksum(offsets: np.ndarray, tokens: np.ndarray) -> str:
     """64-bit digest of a CSR batch, logged so GPU and oracle provably read the same bytes."""
     h = hashlib.blake2b(digest_size=8)

@@ -381,3 +381,19 @@ print("ok")
         full.pop(k, None)
     out = subprocess.run([sys.executable, "-c", code], env=full, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_gpu_known_answers():
+    """The CUDA path against the known-answer vectors of the documented conventions
+    (tests/golden/conventions_kat.json, pinned to the independent micro-oracle)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "conventions_kat.json")) as f:
+        kat = json.load(f)
+    for row in kat["signature"]:
+        off, tok = csr([row["ids"]])
+        d_off, d_tok = to_dev(off, tok)
+        idx = LSHBloom(row["num_perm"], row["b"], row["r"], 1000, 1e-5, row["seed"], device=0)
+        assert u32(idx.signatures(d_off, d_tok))[0].tolist() == row["sig"]
+        assert u64(idx.band_hashes(d_off, d_tok))[0].tolist() == [int(x, 16) for x in row["band_hashes"]]
+        idx.close()
