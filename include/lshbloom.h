@@ -62,6 +62,7 @@ extern "C" {
 #define LSHBLOOM_MAX_BANDS 64   /* bands per handle */
 #define LSHBLOOM_MAX_PERM 1024  /* num_perm */
 #define LSHBLOOM_MAX_K 64       /* probes per band hash (p >= ~5e-20) */
+#define LSHBLOOM_NSTAGES 3      /* lshbloom_stage_times entries */
 
 typedef struct lshbloom lshbloom; /* opaque */
 
@@ -98,7 +99,31 @@ typedef struct {
                             not depend on it */
     uint32_t index_kind; /* LSHBLOOM_INDEX_BLOOM (0, the paper's method),
                             LSHBLOOM_INDEX_CLASSIC (1) or LSHBLOOM_INDEX_BLOCKED (2); see below */
+    uint32_t bloom_path; /* how a batch is applied to Bloom filters (results never depend on it):
+                            LSHBLOOM_PATH_AUTO (0), _RANDOM (1) or _SWEEP (2); see below */
+    uint32_t sweep_log2_window; /* sweep window 2^w bits, w in [10, 19] (0 = chosen per batch) */
+    uint32_t sweep_cap;  /* sweep records per bin before the exact layout (0 = from the batch's
+                            expected load; tests use tiny values to force the exact layout) */
 } lshbloom_config;
+
+/* Bloom paths.  Both evaluate the same stream-order rule -- bit g of band j is set before
+ * document i iff it was set before the batch or some earlier document of the batch probes g
+ * (every document inserts all its band hashes) -- and give identical results:
+ * LSHBLOOM_PATH_RANDOM: per sub-batch of documents, every probe reads and atomically sets its
+ *   filter word in place (K3-K6): the fast form while the filters fit in L2 (<= ~64 MB) or a
+ *   batch probes few lines of large filters.
+ * LSHBLOOM_PATH_SWEEP: probes are binned by filter window (2^w bits), then every touched window
+ *   is copied HBM -> shared memory once (TMA bulk copy), updated there for all of its probes,
+ *   and written back once (K7-K9): one read + one write per touched filter line per batch
+ *   instead of two random 128-byte line fetches per probe -- the fast form for dense batches on
+ *   HBM-resident filters (C3-C5).  Batches of more than 4,194,304 documents are swept in
+ *   pieces of that size.
+ * LSHBLOOM_PATH_AUTO: the sweep when the owned filters exceed 96 MB and a batch puts at least
+ *   256 probes per 64 KB window, else random access.  (Environment LSHBLOOM_BLOOM_PATH =
+ *   random|sweep overrides AUTO for experiments.) */
+#define LSHBLOOM_PATH_AUTO 0
+#define LSHBLOOM_PATH_RANDOM 1
+#define LSHBLOOM_PATH_SWEEP 2
 
 /* Index kinds.
  * LSHBLOOM_INDEX_BLOOM: one Bloom filter per band -- the paper's method.
@@ -129,7 +154,9 @@ typedef struct {
     uint32_t k;               /* probes per band hash */
     uint32_t num_perm, b, r, shingle_n;
     uint32_t band_lo, band_hi;/* owned bands (global indices) */
-    uint64_t words_per_band;  /* uint32 words per filter = 2*ceil(m/64) */
+    uint64_t words_per_band;  /* uint32 words per filter = 4*ceil(m/128): the S:314 storage
+                                 rounded up to 16 bytes (TMA bulk-copy granularity); padding bits
+                                 are never set */
     uint64_t filter_bytes;    /* device bytes of the owned filters */
     double p_eff;             /* 1-(1-p)^b */
     uint64_t doc_count;       /* documents inserted so far */
@@ -139,6 +166,7 @@ typedef struct {
     double fp_rate;
     uint32_t index_kind;      /* LSHBLOOM_INDEX_BLOOM / _CLASSIC / _BLOCKED */
     uint64_t classic_slots;   /* classic: table slots per band (0 for Bloom) */
+    uint64_t sweeps;          /* batches (or 4M-document pieces) applied by the sweep path */
 } lshbloom_info_t;
 
 /* Create an index of b Bloom filters: sizes them from (n_expected, fp_rate),
@@ -216,10 +244,11 @@ LSHBLOOM_API int lshbloom_info(const lshbloom *h, lshbloom_info_t *out);
 /* Last error message of h (or of the last failed create when h is NULL). */
 LSHBLOOM_API const char *lshbloom_last_error(const lshbloom *h);
 
-/* Stage timing with CUDA events recorded on the call's stream around the MinHash (K1)
- * launches and the Bloom (K3-K6) sub-batch loop.  enable != 0 turns recording on for later
- * calls.  ms_out[0] / ms_out[1] receive the K1 / Bloom milliseconds accumulated since the
- * previous read, n_out[0] / n_out[1] the number of timed K1 launches / Bloom stages; both
+/* Stage timing with CUDA events recorded around the MinHash (K1) launches, the Bloom stage
+ * (K3-K6 sub-batch loop, or the sweep path's binning + sweep, on the Bloom stream) and the
+ * sweep path's final kernels (exact-layout fix-up, window sweep, verdict).  enable != 0 turns
+ * recording on for later calls.  ms_out[0..LSHBLOOM_NSTAGES) receive the K1 / Bloom / sweep
+ * milliseconds accumulated since the previous read, n_out[] the number of timed stages; the
  * accumulators are then reset.  Either pointer may be NULL. */
 LSHBLOOM_API int lshbloom_stage_times(lshbloom *h, int32_t enable, double *ms_out, uint64_t *n_out);
 

@@ -16,6 +16,8 @@ _LIB_PATH = os.environ.get("LSHBLOOM_LIB") or os.path.join(os.path.dirname(os.pa
                                                            "liblshbloom.so")
 
 OK, EUSAGE, EDATA, ERUNTIME, ENOMEM, EFORMAT, ETRUNC, ECHECKSUM, EIO = range(9)
+NSTAGES = 3                      # LSHBLOOM_NSTAGES: K1, Bloom stage, sweep kernels
+BLOOM_PATHS = {"auto": 0, "random": 1, "sweep": 2}
 
 
 class LSHBloomError(RuntimeError):
@@ -35,7 +37,9 @@ class _Config(ctypes.Structure):
                 ("shingle_n", ctypes.c_uint32), ("n_expected", ctypes.c_uint64),
                 ("fp_rate", ctypes.c_double), ("seed", ctypes.c_uint64),
                 ("device", ctypes.c_int32), ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32),
-                ("sub_batch", ctypes.c_uint32), ("index_kind", ctypes.c_uint32)]
+                ("sub_batch", ctypes.c_uint32), ("index_kind", ctypes.c_uint32),
+                ("bloom_path", ctypes.c_uint32), ("sweep_log2_window", ctypes.c_uint32),
+                ("sweep_cap", ctypes.c_uint32)]
 
 
 class _Info(ctypes.Structure):
@@ -46,7 +50,8 @@ class _Info(ctypes.Structure):
                 ("p_eff", ctypes.c_double), ("doc_count", ctypes.c_uint64),
                 ("oversubscribed", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("n_expected", ctypes.c_uint64), ("fp_rate", ctypes.c_double),
-                ("index_kind", ctypes.c_uint32), ("classic_slots", ctypes.c_uint64)]
+                ("index_kind", ctypes.c_uint32), ("classic_slots", ctypes.c_uint64),
+                ("sweeps", ctypes.c_uint64)]
 
 
 class _Plan(ctypes.Structure):
@@ -112,15 +117,43 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def _raw(x, kind: str):
-    """(pointer, on_device, keepalive) for a contiguous tensor / array of 4- or 8-byte ints."""
+_INT_KINDS = "iu"
+
+
+def _raw(x, kind: str, itemsize: int | None = None):
+    """(pointer, on_device, keepalive) for a contiguous tensor / array of integers; `itemsize`
+    (bytes per element) is enforced when given -- the library reads offsets as u64 and tokens as
+    u32, so e.g. numpy's default int64 token array would otherwise be misread silently."""
     if _is_torch(x):
-        import torch
         if not x.is_contiguous():
             raise ValueError("%s must be contiguous" % kind)
+        if x.dtype.is_floating_point or x.dtype.is_complex or x.dtype == __import__("torch").bool:
+            raise TypeError("%s must be an integer tensor, got %s" % (kind, x.dtype))
+        if itemsize is not None and x.element_size() != itemsize:
+            raise TypeError("%s must have %d-byte elements, got %s" % (kind, itemsize, x.dtype))
         return x.data_ptr(), (1 if x.is_cuda else 0), x
     a = np.ascontiguousarray(x)
+    if a.dtype.kind not in _INT_KINDS:
+        raise TypeError("%s must be an integer array, got %s" % (kind, a.dtype))
+    if itemsize is not None and a.dtype.itemsize != itemsize:
+        raise TypeError("%s must have %d-byte elements, got %s" % (kind, itemsize, a.dtype))
     return a.ctypes.data, 0, a
+
+
+def _check_out(out, n: int, itemsize: int, on_device: bool, kind: str = "out"):
+    """A caller-supplied output: contiguous, `n` elements of `itemsize` bytes, in the batch's
+    memory space."""
+    if _is_torch(out):
+        ok = out.is_contiguous() and out.numel() == n and out.element_size() == itemsize
+        dev = out.is_cuda
+    else:
+        ok = isinstance(out, np.ndarray) and out.flags.c_contiguous and out.size == n and \
+            out.dtype.itemsize == itemsize and out.dtype.kind in _INT_KINDS
+        dev = False
+    if not ok:
+        raise ValueError("%s must be a contiguous buffer of %d %d-byte integers" % (kind, n, itemsize))
+    if dev != on_device:
+        raise ValueError("%s must live in the same memory space as the inputs" % kind)
 
 
 class LSHBloom:
@@ -132,10 +165,14 @@ class LSHBloom:
 
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, shingle_n: int = 5, device: int | None = None, rank: int = 0, world: int = 1,
-                 sub_batch: int = 0, index: str = "bloom", _handle=None):
+                 sub_batch: int = 0, index: str = "bloom", bloom_path: str = "auto", sweep_window_log2: int = 0,
+                 sweep_cap: int = 0, _handle=None):
         """index: "bloom" (the paper's per-band Bloom filters), "classic" (the exact
         band-equality MinHashLSH index it replaces; fp_rate is ignored) or "blocked" (a blocked
-        Bloom variant: all k probes of a band hash in one 1024-bit block)."""
+        Bloom variant: all k probes of a band hash in one 1024-bit block).
+        bloom_path: "auto", "random" (K3-K6, random access per probe) or "sweep" (K7-K9, windows
+        streamed through shared memory); results are identical.  sweep_window_log2 / sweep_cap
+        override the sweep's window size (2^w bits, w in [10, 19]) and bin capacity."""
         self._lib = lib()
         kinds = {"bloom": 0, "classic": 1, "blocked": 2}
         if index not in kinds:
@@ -147,8 +184,11 @@ class LSHBloom:
             except Exception:
                 device = -1
         if _handle is None:
+            if bloom_path not in BLOOM_PATHS:
+                raise ValueError("bloom_path must be 'auto', 'random' or 'sweep'")
             cfg = _Config(num_perm, b, r, shingle_n, n_expected, fp_rate, seed & (2**64 - 1), device,
-                          rank, world, sub_batch, kinds[index])
+                          rank, world, sub_batch, kinds[index], BLOOM_PATHS[bloom_path], sweep_window_log2,
+                          sweep_cap)
             h = ctypes.c_void_p()
             rc = self._lib.lshbloom_create_ex(ctypes.byref(cfg), ctypes.byref(h))
             if rc:
@@ -175,8 +215,8 @@ class LSHBloom:
             raise LSHBloomError(rc, self._lib.lshbloom_last_error(self._h).decode())
 
     def _batch(self, offsets, tokens, stream):
-        po, do, ko = _raw(offsets, "offsets")
-        pt, dt, kt = _raw(tokens, "tokens")
+        po, do, ko = _raw(offsets, "offsets", 8)
+        pt, dt, kt = _raw(tokens, "tokens", 4)
         if do != dt:
             raise ValueError("offsets and tokens must live in the same memory space")
         n = (offsets.numel() if _is_torch(offsets) else len(ko)) - 1
@@ -218,11 +258,14 @@ class LSHBloom:
         self._check(self._lib.lshbloom_band_hashes_sharded(self._h, ctypes.byref(bt), self._ptr(out)))
         return out
 
-    def stage_times(self, enable: bool = True):
-        """(K1 ms, Bloom ms), (K1 launches, Bloom stages) since the last read; resets them."""
-        ms = (ctypes.c_double * 2)()
-        nn = (ctypes.c_uint64 * 2)()
+    def stage_times(self, enable: bool = True, all_stages: bool = False):
+        """(K1 ms, Bloom ms), (K1 launches, Bloom stages) since the last read; resets them.
+        all_stages: also the sweep kernels' ms / count (third entries)."""
+        ms = (ctypes.c_double * NSTAGES)()
+        nn = (ctypes.c_uint64 * NSTAGES)()
         self._check(self._lib.lshbloom_stage_times(self._h, 1 if enable else 0, ms, nn))
+        if all_stages:
+            return tuple(ms), tuple(nn)
         return (ms[0], ms[1]), (nn[0], nn[1])
 
     def query_insert(self, offsets, tokens, *, out=None, stream=None):
@@ -230,15 +273,21 @@ class LSHBloom:
         bt, keep, n, dev = self._batch(offsets, tokens, stream)
         if out is None:
             out = self._out((n,), np.uint8, _torch_dtype("uint8"), dev, offsets)
+        else:
+            _check_out(out, n, 1, dev)
         self._check(self._lib.lshbloom_query_insert(self._h, ctypes.byref(bt), self._ptr(out)))
         return out
 
     def query_insert_bands(self, bh_owned, *, out=None, stream=None):
         """Bloom stage only: bh_owned [n][band_hi-band_lo] -> hit flags [n] (OR over owned bands)."""
-        p, dev, keep = _raw(bh_owned, "bh_owned")
+        p, dev, keep = _raw(bh_owned, "bh_owned", 8)
+        if tuple(bh_owned.shape) != (bh_owned.shape[0], self.band_hi - self.band_lo):
+            raise ValueError("bh_owned must be [n][%d] (the owned bands)" % (self.band_hi - self.band_lo))
         n = bh_owned.shape[0]
         if out is None:
             out = self._out((n,), np.uint8, _torch_dtype("uint8"), dev, bh_owned)
+        else:
+            _check_out(out, n, 1, bool(dev))
         if stream is None and dev:
             import torch
             stream = torch.cuda.current_stream(bh_owned.device).cuda_stream
@@ -256,7 +305,7 @@ class LSHBloom:
     def query_insert_bands_peers(self, bh_owned, doc_start, peer_flags, *, stream=None):
         """Bloom stage of the owned bands for all documents of the global batch, raising each hit
         document's flag in its home rank's buffer (peer_flags: `world` device pointers)."""
-        p, dev, keep = _raw(bh_owned, "bh_owned")
+        p, dev, keep = _raw(bh_owned, "bh_owned", 8)
         if not dev:
             raise ValueError("bh_owned must be a device tensor")
         n = int(doc_start[-1])

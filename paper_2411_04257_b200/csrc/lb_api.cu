@@ -80,12 +80,17 @@ struct lshbloom {
   uint64_t* d_ckeys = nullptr;    // [bl][2^c_log2cap]
   uint64_t* d_cvals = nullptr;
   uint32_t c_log2cap = 0;
-  // stage timing (lshbloom_stage_times)
+  // window-sweep Bloom stage (lb_sweep.cu)
+  uint32_t bloom_path = 0;        // LSHBLOOM_PATH_AUTO / _RANDOM / _SWEEP
+  uint32_t sweep_wb_force = 0, sweep_cap_force = 0;
+  DevBuf sw_cursor, sw_cursor2, sw_start, sw_rec, sw_miss, sw_eg;
+  uint64_t sweeps = 0;            // sweeps run (lshbloom_info)
+  // stage timing (lshbloom_stage_times): K1, Bloom stage, sweep kernels (K7x-K9)
   bool timing = false;
-  cudaEvent_t tev[4] = {nullptr, nullptr, nullptr, nullptr};
-  bool pend[2] = {false, false};
-  double stage_ms[2] = {0, 0};
-  uint64_t stage_n[2] = {0, 0};
+  cudaEvent_t tev[2 * LSHBLOOM_NSTAGES] = {};
+  bool pend[LSHBLOOM_NSTAGES] = {};
+  double stage_ms[LSHBLOOM_NSTAGES] = {};
+  uint64_t stage_n[LSHBLOOM_NSTAGES] = {};
   std::string err;
   bool poisoned = false;
 };
@@ -138,11 +143,12 @@ void free_all(lshbloom* h) {
   F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_clist); F(h->d_cb); F(h->d_ekey);
   F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->tok[2].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
+  F(h->sw_cursor.p); F(h->sw_cursor2.p); F(h->sw_start.p); F(h->sw_rec.p); F(h->sw_miss.p); F(h->sw_eg.p);
   for (int i = 0; i < 3; i++) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
   }
-  for (int i = 0; i < 4; i++)
+  for (int i = 0; i < 2 * LSHBLOOM_NSTAGES; i++)
     if (h->tev[i]) cudaEventDestroy(h->tev[i]);
   if (h->ev_fuse) cudaEventDestroy(h->ev_fuse);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -182,7 +188,7 @@ void stage_end(lshbloom* h, int st, cudaStream_t s) {
 }
 // after the stream is synchronised
 void stage_collect(lshbloom* h) {
-  for (int st = 0; st < 2; st++) {
+  for (int st = 0; st < LSHBLOOM_NSTAGES; st++) {
     if (!h->pend[st]) continue;
     float ms = 0;
     if (cudaEventElapsedTime(&ms, h->tev[2 * st], h->tev[2 * st + 1]) == cudaSuccess) {
@@ -396,11 +402,9 @@ int classic_capacity(lshbloom* h, uint64_t n) {
   return LSHBLOOM_OK;
 }
 
-// K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
-int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin, uint64_t i_end,
-              uint8_t* dup_dev, cudaStream_t s, bool first = true, bool last = true, const DupSink* peers = nullptr) {
-  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC)
-    return run_classic(h, bh_dev, bh_sj, bh_si, i_begin, i_end, dup_dev, s, first, last, peers);
+// Filter geometry, seeds, band-hash layout and flag sink of a Bloom launch.
+BloomParams bloom_params(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint8_t* dup_dev,
+                         const DupSink* peers) {
   BloomParams p;
   memset(&p, 0, sizeof p);
   p.F = h->d_F;
@@ -431,6 +435,16 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
   if (peers) p.dup = *peers;
   else p.dup.local = dup_dev;
   p.err = &h->d_err->pad;
+  return p;
+}
+
+// K3-K6 over bh_dev[n][bl] in sub-batches; dup_dev[n] must be zeroed by the caller.
+int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t i_begin, uint64_t i_end,
+              uint8_t* dup_dev, cudaStream_t s, bool first = true, bool last = true, const DupSink* peers = nullptr) {
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC)
+    return run_classic(h, bh_dev, bh_sj, bh_si, i_begin, i_end, dup_dev, s, first, last, peers);
+  BloomParams p = bloom_params(h, bh_dev, bh_sj, bh_si, dup_dev, peers);
+  const uint64_t SB = h->sub_batch;
   if (first) stage_begin(h, 1, s);
   for (uint64_t i0 = i_begin; i0 < i_end; i0 += SB) {
     if (h->gen >= kGenMax) {   // generation tags exhausted: clear E once every ~4M sub-batches
@@ -442,7 +456,6 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
     p.gen = h->gen++;
     const uint64_t qslots = 1ull << h->q_log2;
     p.Q = h->d_Q + (p.gen & 1) * qslots;
-    p.Q_prev = h->d_Q + ((p.gen + 1) & 1) * qslots;
     p.i0 = (uint32_t)i0;
     p.nsb = (uint32_t)std::min<uint64_t>(SB, i_end - i0);
     h->launches += launch_bloom_subbatch(p, h->sm_count, s);
@@ -450,6 +463,131 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
   }
   if (last) stage_end(h, 1, s);
   return LSHBLOOM_OK;
+}
+
+// ------------------------------------------------------------------ window-sweep Bloom path
+
+constexpr uint64_t kSweepMaxDocs = 1ull << 22;   // documents per sweep (records carry 32-bit
+                                                 // document offsets; path (b) keeps 32-bit minima)
+
+struct SweepPlan {
+  bool use = false;
+  uint32_t wb = 0, cap = 0;
+  uint64_t nw = 0, nbins = 0, piece = 0;
+};
+
+// Window size and bin capacity for a batch of n documents (pieces of <= kSweepMaxDocs): the
+// largest window whose expected load mu = n k 2^wb / m stays <= 1536 records (so a bin of
+// mu + 7 sqrt(mu) + 64 fits the K8 CTA's 2048 register-held records), and whether the sweep
+// beats random access (AUTO: owned filters beyond 96 MB, i.e. not L2-resident, and >= 256
+// probes per 64 KB window).
+SweepPlan plan_sweep(const lshbloom* h, uint64_t n) {
+  SweepPlan sp;
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC || h->bloom_path == LSHBLOOM_PATH_RANDOM || n == 0) return sp;
+  sp.piece = std::min<uint64_t>(n, kSweepMaxDocs);
+  const double rho = (double)sp.piece * h->k / (double)h->m;      // records per filter bit
+  uint32_t wb = 10;
+  while (wb < 19 && rho * (double)(1ull << (wb + 1)) <= 1536.0) wb++;
+  if (h->sweep_wb_force) wb = h->sweep_wb_force;
+  if (h->bloom_path == LSHBLOOM_PATH_AUTO) {
+    const double fbytes = (double)h->bl * (double)h->W * 4.0;
+    if (!(fbytes > 96e6 && rho * 524288.0 >= 256.0 && rho * 1024.0 <= 1536.0)) return sp;
+  }
+  const double mu = rho * (double)(1ull << wb);
+  sp.use = true;
+  sp.wb = wb;
+  sp.cap = h->sweep_cap_force ? h->sweep_cap_force : (uint32_t)std::ceil(mu + 7.0 * std::sqrt(mu) + 64.0);
+  sp.nw = (h->m + (1ull << wb) - 1) >> wb;
+  sp.nbins = sp.nw * h->bl;
+  return sp;
+}
+
+// ensure() for buffers that must start zeroed (the miss words are re-zeroed by K9 after use).
+int ensure_zeroed(lshbloom* h, DevBuf& b, size_t bytes, cudaStream_t s) {
+  void* before = b.p;
+  LB_CUDA(h, ensure(b, bytes));
+  if (b.p != before) LB_CUDA(h, cudaMemsetAsync(b.p, 0, b.cap, s));
+  return LSHBLOOM_OK;
+}
+
+int sweep_alloc(lshbloom* h, const SweepPlan& sp, cudaStream_t s) {
+  const uint64_t recs = std::max<uint64_t>(sp.nbins * sp.cap, sp.piece * h->k * h->bl);
+  LB_CUDA(h, ensure(h->sw_cursor, sp.nbins * 4));
+  LB_CUDA(h, ensure(h->sw_cursor2, sp.nbins * 4));
+  LB_CUDA(h, ensure(h->sw_start, (sp.nbins + 1) * 8));
+  LB_CUDA(h, ensure(h->sw_rec, recs * 8));
+  int rc = ensure_zeroed(h, h->sw_miss, sp.piece * 8, s);
+  if (rc) return rc;
+  LB_CUDA(h, ensure(h->sw_eg, (size_t)sweep_grid(h->sm_count, sp.wb) << sp.wb << 2));
+  return LSHBLOOM_OK;
+}
+
+SweepParams sweep_params(lshbloom* h, const SweepPlan& sp, const BloomParams& g, uint64_t i0, uint64_t n) {
+  SweepParams p;
+  memset(&p, 0, sizeof p);
+  p.g = g;
+  p.wb = sp.wb;
+  p.cap = sp.cap;
+  p.nw = sp.nw;
+  p.nbins = sp.nbins;
+  p.cursor = (uint32_t*)h->sw_cursor.p;
+  p.cursor2 = (uint32_t*)h->sw_cursor2.p;
+  p.start = (uint64_t*)h->sw_start.p;
+  p.rec = (uint64_t*)h->sw_rec.p;
+  p.ovf = h->d_counters + 14;
+  p.miss = (uint64_t*)h->sw_miss.p;
+  p.eg = (uint32_t*)h->sw_eg.p;
+  p.i0 = (uint32_t)i0;
+  p.n = (uint32_t)n;
+  return p;
+}
+
+int sweep_begin(lshbloom* h, const SweepParams& p, cudaStream_t s) {
+  LB_CUDA(h, cudaMemsetAsync(p.cursor, 0, p.nbins * 4, s));
+  LB_CUDA(h, cudaMemsetAsync(p.ovf, 0, 4, s));
+  return LSHBLOOM_OK;
+}
+
+int sweep_bin(lshbloom* h, const SweepParams& p, uint64_t lo, uint64_t hi, cudaStream_t s) {
+  h->launches += launch_sweep_bin(p, (uint32_t)lo, (uint32_t)hi, s);
+  LB_CUDA(h, cudaGetLastError());
+  return LSHBLOOM_OK;
+}
+
+int sweep_finish(lshbloom* h, const SweepParams& p, cudaStream_t s, bool first, bool last) {
+  if (first) stage_begin(h, 2, s);
+  h->launches += launch_sweep_finish(p, sweep_grid(h->sm_count, p.wb), s);
+  LB_CUDA(h, cudaGetLastError());
+  if (last) stage_end(h, 2, s);
+  h->sweeps++;
+  return LSHBLOOM_OK;
+}
+
+// The sweep path over band hashes that already exist (query_insert_bands): pieces of
+// <= kSweepMaxDocs documents, each binned then swept.
+int run_bloom_sweep(lshbloom* h, const SweepPlan& sp, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si,
+                    uint64_t n, uint8_t* dup_dev, cudaStream_t s, const DupSink* peers) {
+  int rc = sweep_alloc(h, sp, s);
+  if (rc) return rc;
+  const BloomParams g = bloom_params(h, bh_dev, bh_sj, bh_si, dup_dev, peers);
+  stage_begin(h, 1, s);
+  for (uint64_t i0 = 0; i0 < n; i0 += kSweepMaxDocs) {
+    const uint64_t i1 = std::min(n, i0 + kSweepMaxDocs);
+    const SweepParams p = sweep_params(h, sp, g, i0, i1 - i0);
+    if ((rc = sweep_begin(h, p, s)) || (rc = sweep_bin(h, p, i0, i1, s)) ||
+        (rc = sweep_finish(h, p, s, i0 == 0, i1 == n)))
+      return rc;
+  }
+  stage_end(h, 1, s);
+  return LSHBLOOM_OK;
+}
+
+// The Bloom stage over bh_dev for documents [0, n): sweep or random access (results identical).
+int run_bloom_any(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_si, uint64_t n,
+                  uint8_t* dup_dev, cudaStream_t s, const DupSink* peers = nullptr) {
+  const SweepPlan sp = plan_sweep(h, n);
+  if (sp.use) return run_bloom_sweep(h, sp, bh_dev, bh_sj, bh_si, n, dup_dev, s, peers);
+  return run_bloom(h, bh_dev, bh_sj, bh_si, 0, n, dup_dev, s, true, true, peers);
 }
 
 // query_insert: K1 over document chunks (alternately on the caller's stream s and k1_stream2),
@@ -508,9 +646,57 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     LB_CUDA(h, ensure(h->part, (6 * (size_t)b->n_docs + 6) * sizeof(uint32_t)));
   p.bh_out = bh;
   p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
+  const uint64_t chunk_tokens = b->on_device ? 0 : kChunkTokens;
+  if (!b->on_device && b->offsets[0] != 0) return fail(h, LSHBLOOM_EUSAGE, "offsets[0] must be 0");
+  // Bloom path: with the sweep, each chunk's probes are binned right after its K1 (overlapping
+  // the next chunk's K1) and every piece of <= kSweepMaxDocs documents is swept once complete;
+  // chunk boundaries fall on piece boundaries.
+  const SweepPlan sp = plan_sweep(h, n);
+  auto clip = [&](uint64_t d0, uint64_t d1) {
+    return sp.use ? std::min(d1, (d0 / kSweepMaxDocs + 1) * kSweepMaxDocs) : d1;
+  };
+  // Chunk bounds first, all of them checked before anything is enqueued: a host batch's copies
+  // read tokens [offsets[d0], offsets[d1]) of the caller's buffer, so every bound must satisfy
+  // 0 <= t0 <= t1 <= offsets[n] (the rest of the CSR is validated on the device by K0, which gates
+  // every kernel before any filter mutation).
+  std::vector<std::pair<uint64_t, uint64_t>> chunks;
+  {
+    uint64_t d0 = 0;
+    while (d0 < n) {
+      uint64_t d1;
+      if (b->on_device) {
+        d1 = clip(d0, fuse_chunk_end(d0, n, h->npl));
+      } else {
+        const uint64_t t0 = b->offsets[d0];
+        const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
+        d1 = (uint64_t)(lim - b->offsets) - 1;
+        // at least ~3.5 documents per resident K1 warp (8192 on 148 SMs), however long the
+        // documents: with full-text lengths 64 MB is ~1.7 documents per warp and a chunk would last
+        // as long as its slowest warp (C3 e2e: 155 vs 66 ms per 100K documents).  With the two K1
+        // streams the next chunk fills that tail, so the floor is lower than with one stream (16
+        // per warp): C3 e2e 71.8 -> 70.0 ms per 100K, C4 36.5 -> 35.7 ms per 200K (2K-16K swept).
+        static const uint64_t env_min_docs = [] {
+          const char* e = getenv("LSHBLOOM_HOST_MIN_DOCS");
+          return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) : 0;
+        }();
+        const uint64_t min_docs =
+            env_min_docs ? env_min_docs : (7ull * h->sm_count * 2 * (K1_THREADS_HOST / 32) + 1) / 2;
+        d1 = std::max(d1, std::min(n, d0 + min_docs));
+        if (d1 <= d0) d1 = d0 + 1;
+        d1 = clip(d0, std::min(d1, fuse_chunk_end(d0, n, h->npl)));
+        const uint64_t t1 = b->offsets[d1];
+        if (t1 < t0 || t1 > b->offsets[n])
+          return fail(h, LSHBLOOM_EUSAGE, "malformed offsets near index " + std::to_string(d0) +
+                                              " (decreasing, or beyond offsets[n_docs])");
+      }
+      chunks.emplace_back(d0, d1);
+      d0 = d1;
+    }
+  }
   int rc = reset_err(h, s);
   if (rc) return rc;
-  uint64_t chunk_tokens = 0;
+  if (sp.use && (rc = sweep_alloc(h, sp, s))) return rc;
+  const BloomParams bp = bloom_params(h, bh, n, 1, ddup, nullptr);
   int nbuf = 2;
   if (b->on_device) {
     h->launches += launch_validate(b->offsets, n, h->d_err, s);
@@ -519,12 +705,10 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     p.tok_base = 0;
   } else {
     // No O(n) host pass: the offsets are validated on the device (K0), which gates every kernel;
-    // the host only checks what its own copies depend on (offsets[0], chunk bounds).
-    if (b->offsets[0] != 0) return fail(h, LSHBLOOM_EUSAGE, "offsets[0] must be 0");
+    // the host only checked what its own copies depend on (offsets[0], chunk bounds, above).
     LB_CUDA(h, ensure(h->off, (n + 1) * sizeof(uint64_t)));
     LB_CUDA(h, cudaMemcpyAsync(h->off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     h->launches += launch_validate((const uint64_t*)h->off.p, n, h->d_err, s);
-    chunk_tokens = kChunkTokens;
     nbuf = host_bufs(n, b->offsets[n]);
     const uint64_t buf_tokens = std::max<uint64_t>(1, std::min(chunk_tokens, b->offsets[n]));
     for (int i = 0; i < nbuf; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
@@ -540,34 +724,12 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
   const int nks = alt ? h->k1_nstreams : 1;
   cudaStream_t kst[3] = {s, h->k1_stream2, h->k1_stream3};
   for (int k = 1; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_fuse, 0));
-  uint64_t d0 = 0;
   int c = 0;
   stage_begin(h, 0, s);
-  while (d0 < n) {
-    uint64_t d1;
-    if (b->on_device) {
-      d1 = fuse_chunk_end(d0, n, h->npl);
-    } else {
-      const uint64_t t0 = b->offsets[d0];
-      const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
-      d1 = (uint64_t)(lim - b->offsets) - 1;
-      // at least ~3.5 documents per resident K1 warp (8192 on 148 SMs), however long the
-      // documents: with full-text lengths 64 MB is ~1.7 documents per warp and a chunk would last
-      // as long as its slowest warp (C3 e2e: 155 vs 66 ms per 100K documents).  With the two K1
-      // streams the next chunk fills that tail, so the floor is lower than with one stream (16
-      // per warp): C3 e2e 71.8 -> 70.0 ms per 100K, C4 36.5 -> 35.7 ms per 200K (2K-16K swept).
-      // The staging buffers grow to fit.
-      static const uint64_t env_min_docs = [] {
-        const char* e = getenv("LSHBLOOM_HOST_MIN_DOCS");
-        return e ? std::max<uint64_t>(1, strtoull(e, nullptr, 10)) : 0;
-      }();
-      const uint64_t min_docs =
-          env_min_docs ? env_min_docs : (7ull * h->sm_count * 2 * (K1_THREADS_HOST / 32) + 1) / 2;
-      d1 = std::max(d1, std::min(n, d0 + min_docs));
-      if (d1 <= d0) d1 = d0 + 1;
-      d1 = std::min(d1, fuse_chunk_end(d0, n, h->npl));
-      const uint64_t t1 = b->offsets[d1];
-      if (t1 < t0) return fail(h, LSHBLOOM_EUSAGE, "offsets decrease near index " + std::to_string(d0));
+  for (const auto& ch : chunks) {
+    const uint64_t d0 = ch.first, d1 = ch.second;
+    if (!b->on_device) {
+      const uint64_t t0 = b->offsets[d0], t1 = b->offsets[d1];
       const int buf = c % nbuf;
       if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // a chunk larger than the buffer
         LB_CUDA(h, cudaEventSynchronize(h->ev_k1[buf]));   // its last reader is done
@@ -606,8 +768,17 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       stage_end(h, 0, s);
     }
     LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
-    if ((rc = run_bloom(h, bh, n, 1, d0, d1, ddup, h->bloom_stream, d0 == 0, d1 == n))) return rc;
-    d0 = d1;
+    if (!sp.use) {
+      if ((rc = run_bloom(h, bh, n, 1, d0, d1, ddup, h->bloom_stream, d0 == 0, d1 == n))) return rc;
+    } else {
+      const uint64_t p0 = d0 / kSweepMaxDocs * kSweepMaxDocs, p1 = std::min(n, p0 + kSweepMaxDocs);
+      const SweepParams sw = sweep_params(h, sp, bp, p0, p1 - p0);
+      if (d0 == 0) stage_begin(h, 1, h->bloom_stream);
+      if (d0 == p0 && (rc = sweep_begin(h, sw, h->bloom_stream))) return rc;
+      if ((rc = sweep_bin(h, sw, d0, d1, h->bloom_stream))) return rc;
+      if (d1 == p1 && (rc = sweep_finish(h, sw, h->bloom_stream, p0 == 0, p1 == n))) return rc;
+      if (d1 == n) stage_end(h, 1, h->bloom_stream);
+    }
     c++;
   }
   LB_CUDA(h, cudaEventRecord(h->ev_fuse, h->bloom_stream));
@@ -659,6 +830,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     return fail(nullptr, LSHBLOOM_EUSAGE, "index_kind must be 0 (Bloom), 1 (classic) or 2 (blocked Bloom)");
   const bool classic = c.index_kind == LSHBLOOM_INDEX_CLASSIC;
   if (!classic && !(c.fp_rate > 0.0 && c.fp_rate < 1.0)) return fail(nullptr, LSHBLOOM_EUSAGE, "fp_rate must be in (0, 1) (S:273)");
+  if (c.bloom_path > LSHBLOOM_PATH_SWEEP) return fail(nullptr, LSHBLOOM_EUSAGE, "bloom_path must be 0 (auto), 1 (random) or 2 (sweep)");
+  if (c.sweep_log2_window && (c.sweep_log2_window < 10 || c.sweep_log2_window > 19))
+    return fail(nullptr, LSHBLOOM_EUSAGE, "sweep_log2_window must be 0 or in [10, 19]");
   if (c.world == 0) c.world = 1;
   if (c.rank >= c.world) return fail(nullptr, LSHBLOOM_EUSAGE, "rank must be < world");
   if (c.world > c.b) return fail(nullptr, LSHBLOOM_EUSAGE, "world must be <= b (every rank owns >= 1 band)");
@@ -682,7 +856,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     h->m = h->nb * 1024;
   }
   h->m_inv = ~0ull / h->m;
-  h->W = 2 * ((h->m + 63) / 64);
+  h->W = 4 * ((h->m + 127) / 128);   // S:314 storage rounded up to 16 B (TMA bulk-copy granularity)
   const uint32_t base = c.b / c.world, rem = c.b % c.world;
   h->band_lo = c.rank * base + std::min(c.rank, rem);
   h->bl = base + (c.rank < rem ? 1 : 0);
@@ -691,6 +865,12 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   while (npl * 32 < c.num_perm) npl *= 2;
   h->npl = npl;
   h->sub_batch = c.sub_batch ? std::min<uint32_t>(c.sub_batch, 1u << 22) : kDefaultSubBatch;   // doc offsets: 22 bits in Q
+  h->bloom_path = c.bloom_path;
+  if (h->bloom_path == LSHBLOOM_PATH_AUTO)
+    if (const char* e = getenv("LSHBLOOM_BLOOM_PATH"))
+      h->bloom_path = !strcmp(e, "sweep") ? LSHBLOOM_PATH_SWEEP : !strcmp(e, "random") ? LSHBLOOM_PATH_RANDOM : 0;
+  h->sweep_wb_force = c.sweep_log2_window;
+  h->sweep_cap_force = c.sweep_cap;
 
   int dev = c.device;
   if (dev < 0) cudaGetDevice(&dev);
@@ -732,7 +912,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     CR(cudaEventCreateWithFlags(&h->ev_k1[i], cudaEventDisableTiming));
     CR(cudaEventRecord(h->ev_k1[i], h->own_stream));
   }
-  for (int i = 0; i < 4; i++) CR(cudaEventCreate(&h->tev[i]));
+  for (int i = 0; i < 2 * LSHBLOOM_NSTAGES; i++) CR(cudaEventCreate(&h->tev[i]));
 
   // Hash family (DESIGN R5), in the kernel's limb layout.
   std::vector<PermCoef> coef(32 * npl);
@@ -881,7 +1061,7 @@ int lshbloom_stage_times(lshbloom* h, int32_t enable, double* ms_out, uint64_t* 
   int rc = check_handle(h);
   if (rc) return rc;
   h->timing = enable != 0;
-  for (int st = 0; st < 2; st++) {
+  for (int st = 0; st < LSHBLOOM_NSTAGES; st++) {
     if (ms_out) ms_out[st] = h->stage_ms[st];
     if (n_out) n_out[st] = h->stage_n[st];
     h->stage_ms[st] = 0;
@@ -933,7 +1113,7 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   }
   if ((rc = reset_err(h, s))) return rc;
   LB_CUDA(h, cudaMemsetAsync(dhit, 0, n_docs, s));
-  if ((rc = run_bloom(h, dbh, 1, h->bl, 0, n_docs, dhit, s))) return rc;
+  if ((rc = run_bloom_any(h, dbh, 1, h->bl, n_docs, dhit, s))) return rc;
   if (!on_device) LB_CUDA(h, cudaMemcpyAsync(hit_out, dhit, n_docs, cudaMemcpyDeviceToHost, s));
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n_docs;
@@ -988,7 +1168,7 @@ int lshbloom_query_insert_bands_peers(lshbloom* h, const uint64_t* bh_owned, uin
   DeviceGuard g(h->device);
   cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
   if ((rc = reset_err(h, s))) return rc;
-  if ((rc = run_bloom(h, bh_owned, 1, h->bl, 0, n_global, nullptr, s, true, true, &sink))) return rc;
+  if ((rc = run_bloom_any(h, bh_owned, 1, h->bl, n_global, nullptr, s, &sink))) return rc;
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n_global;
   return LSHBLOOM_OK;
@@ -1022,7 +1202,10 @@ int lshbloom_filter_copy(lshbloom* h, uint32_t j, uint32_t* dst) {
 }
 
 int lshbloom_info(const lshbloom* h, lshbloom_info_t* out) {
-  if (!h || !out) return LSHBLOOM_EUSAGE;
+  if (!h || !out) {
+    g_create_error = "lshbloom_info: NULL handle / output";
+    return LSHBLOOM_EUSAGE;
+  }
   memset(out, 0, sizeof *out);
   out->m = h->m;
   out->k = h->k;
@@ -1041,6 +1224,7 @@ int lshbloom_info(const lshbloom* h, lshbloom_info_t* out) {
   out->n_expected = h->cfg.n_expected;
   out->fp_rate = h->cfg.fp_rate;
   out->index_kind = h->cfg.index_kind;
+  out->sweeps = h->sweeps;
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) {
     out->classic_slots = 1ull << h->c_log2cap;
     out->filter_bytes = ((uint64_t)h->bl << h->c_log2cap) * 16;

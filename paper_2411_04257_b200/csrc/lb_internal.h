@@ -79,7 +79,6 @@ struct MinhashParams {
 struct BloomParams {
   uint32_t* F;               // owned filters, bl * W uint32 words
   uint64_t* Q;               // compact earliest-setter table of this sub-batch (2^q_log2 slots)
-  uint64_t* Q_prev;          // the other buffer (previous sub-batch)
   uint32_t q_log2;
   uint64_t W;                // uint32 words per band
   uint64_t m, m_inv;         // probe modulus and Barrett reciprocal
@@ -103,6 +102,30 @@ struct BloomParams {
   uint32_t cb_log2;
   DupSink dup;               // [n] batch flags (OR over owned bands), local or in peer memory
   const int* err;
+};
+
+// Window-sweep Bloom stage (lb_sweep.cu).  Each band's filter is cut into windows of 2^wb bits;
+// K7 bins every probe of a batch by (band, window) into fixed-capacity bins (records
+// (position in window) << 32 | (document - i0)), K8 streams each non-empty window HBM -> shared
+// memory with a TMA bulk copy, applies all of its records with the stream-order lemma in shared
+// memory and writes the window back (one read + one write of every touched filter line per batch
+// instead of two random line fetches per probe), K9 turns the per-(document, band) miss bits into
+// duplicate flags.  A bin that exceeds its capacity switches the whole sweep to an exact layout
+// (scan of the bin counts + re-scatter), decided on the device.
+struct SweepParams {
+  BloomParams g;             // geometry, seeds, filters, band hashes, dup sink, error gate
+  uint32_t wb;               // log2 window bits (10..19)
+  uint32_t cap;              // records per bin in the fixed-capacity layout
+  uint64_t nw;               // windows per band = ceil(m / 2^wb)
+  uint64_t nbins;            // bl * nw, band-major
+  uint32_t* cursor;          // [nbins] records binned (counts every record, including those beyond cap)
+  uint32_t* cursor2;         // [nbins] exact-layout scatter cursors
+  uint64_t* start;           // [nbins + 1] exact layout: exclusive scan of cursor
+  uint64_t* rec;             // records: fixed layout bin * cap + slot, exact layout start[bin] + slot
+  uint32_t* ovf;             // nonzero: some bin exceeded cap -> exact layout
+  uint64_t* miss;            // [n] bit jl set: band jl of sweep document d missed
+  uint32_t* eg;              // [grid][2^wb] earliest setter per position, for bins beyond 2048 records
+  uint32_t i0, n;            // this sweep = batch documents [i0, i0 + n)
 };
 
 struct ClassicParams {        // classic MinHashLSH index (lb_classic.cu)
@@ -129,5 +152,11 @@ int launch_validate(const uint64_t* offsets, uint64_t n_docs, ErrState* err, cud
 int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps);
 int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s);
 int launch_classic(const ClassicParams& p, cudaStream_t s);
+int launch_sweep_bin(const SweepParams& p, uint32_t lo, uint32_t hi, cudaStream_t s);
+int launch_sweep_finish(const SweepParams& p, int grid, cudaStream_t s);
+int sweep_grid(int sm_count, uint32_t wb);     // K8 CTAs (persistent) for a window size
+constexpr int kSweepThreads = 512;               // K8 block size
+constexpr int kSweepRPT = 4;                     // records per thread held in registers
+constexpr uint32_t kSweepCapReg = kSweepThreads * kSweepRPT;   // 2048: larger bins take the global path
 
 }  // namespace lb

@@ -215,7 +215,7 @@ def test_info_sizing_matches_oracle():
         idx = LSHBloom(128, 16, 8, n, p, 0, device=0, sub_batch=1024)
         inf = idx.info()
         assert (inf["m"], inf["k"]) == oracle.bloom_size(n, p)
-        assert inf["words_per_band"] == 2 * ((inf["m"] + 63) // 64)
+        assert inf["words_per_band"] == 4 * ((inf["m"] + 127) // 128)   # S:314 storage, 16-B rounded
         assert inf["p_eff"] == pytest.approx(1 - (1 - p) ** 16, rel=1e-12)
         idx.close()
 
