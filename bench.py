@@ -1,16 +1,20 @@
 #!/usr/bin/env python3
 """bench.py -- LSHBloom hot path throughput on B200 (documents/s), BASELINE.json's metric.
 
-Workload (N=1): config C2 of BASELINE.json -- 1M abstract-like documents (lognormal(200, 80)
-words, Zipf(1.1) over 200k ids, 10% near-duplicates at Jaccard 0.7-0.99), word 5-grams,
-num_perm=128, b=16, r=8, per-filter fp 1e-5, seed 0.  A step = one pass of the whole hot path
-over the 1M-document batch: zero the filters (a0), then lshbloom_query_insert (shingle
-fingerprints, MinHash, band hashes, k-probe query-then-insert in exact stream order,
-duplicate flags).  N > 1 (torchrun): weak scaling, 1M documents per rank, bands sharded over
-ranks with one NCCL all-to-all + one all-reduce(max) per step (paper_2411_04257_b200.sharded).
+Headline workload (N=1): config C3 of BASELINE.json, the largest configuration that runs on one
+GPU without band sharding -- 8M full-text-like documents (lognormal(4000, 2500) words, Zipf(1.05)
+over 1M ids, 8% near-duplicates), word 5-grams, num_perm=256, b=32, r=8, per-filter fp 1e-5,
+filters sized for the whole corpus (n_expected = 8M: 32 x 24 MB = 767 MB, HBM-resident).  A
+step = one pass of the whole hot path over one 200K-document batch of the stream: zero the
+filters (a0), then lshbloom_query_insert (shingle fingerprints, MinHash, band hashes, k-probe
+query-then-insert in exact stream order, duplicate flags).  N > 1 (torchrun): weak scaling,
+200K documents per rank, bands sharded over ranks (paper_2411_04257_b200.sharded).
 
 `value` is device-resident (inputs already in HBM); `e2e` is the same step through the C-ABI
 with pinned HOST buffers (H2D of the CSR batch and D2H of the flags inside the timed region).
+Secondary lines in the same JSON object: `secondary.C2` (1M abstracts per step, 48 MB of
+L2-resident filters) and `roofline_bloom_hbm` (C5 geometry: 20 x 3.0 GB filters, 4M-document
+stream batches -- the Bloom stage at its HBM-bound worst, alone and inside the fused step).
 `--impl reference` times the CPU oracle (oracle/) on a bounded sample of the same workload.
 """
 from __future__ import annotations
@@ -57,7 +61,8 @@ def parse():
                          "index, or the blocked Bloom variant")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: band-hash / flag exchange over peer memory (default) or NCCL")
-    ap.add_argument("--hbm-docs", type=int, default=1_000_000)
+    ap.add_argument("--hbm-docs", type=int, default=4_000_000, help="C5 leg: documents per stream batch")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the secondary C2 line")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
     a = ap.parse_args()
     if not a.docs:
@@ -140,10 +145,32 @@ def workload(cfg, rank: int, n_docs: int):
     return off, tok, time.time() - t
 
 
-def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5) -> int:
+def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 1024):
+    """(total, on the exact kernel, on the screened kernel) evaluations: S_d x num_perm per
+    document, S_d = max(1, L_d - n + 1).  With 256 permutations the library runs documents of
+    >= split_s shingles on the screened kernel (lb_minhash.cu, LSHBLOOM_K1_SPLIT_S)."""
     L = np.diff(off.astype(np.int64))
     S = np.where(L >= n, L - n + 1, 1)
-    return int(S.sum()) * num_perm
+    total = int(S.sum()) * num_perm
+    if num_perm > 128:
+        long_ = int(S[S >= split_s].sum()) * num_perm
+        return total, total - long_, long_
+    return total, total, 0
+
+
+# K1 issue bounds per evaluation on the fmaheavy pipe (IMAD.WIDE.U32 0.25 warp-instr/clk/SMSP,
+# 32-bit IMAD 0.5; tools/micro/pipe_micro.cu, profiles/pipe_micro.txt): the exact form needs four
+# 32x32->64 products (16 pipe cycles per warp-evaluation -> 2 evaluations/clk/SMSP); the screened
+# form (long documents) decides almost every evaluation from two IMAD.WIDE + two 32-bit IMAD
+# (12 cycles -> 8/3 evaluations/clk/SMSP).
+K1_EVALS_PER_CLK_SMSP = {"exact": 2.0, "screened": 8.0 / 3.0}
+
+
+def k1_peak(evals, f_hz: float, sms: int = 148):
+    """Evaluation-weighted bound (Geval/s) of K1 for a batch split over the two kernels."""
+    total, ex, sc = evals
+    t = (ex / K1_EVALS_PER_CLK_SMSP["exact"] + sc / K1_EVALS_PER_CLK_SMSP["screened"]) / (sms * 4 * f_hz)
+    return total / t
 
 
 def load_traffic(config: str):
@@ -216,84 +243,145 @@ def run_reference(args, cfg):
     return 0
 
 
-# --------------------------------------------------------------------------- HBM-resident Bloom leg
+# --------------------------------------------------------------------------- Bloom stage timing
 
-def hbm_leg(args, torch, dev, peaks, peak_src):
-    """The Bloom stage where it is HBM-bound: C5's index geometry (128 perms, b=20 r=6,
-    n_expected=1e9 -> 20 x 3.0 GB filters, m > 2^32) over C5's first documents, one fused
-    lshbloom_query_insert per step on freshly zeroed filters (every probe sets a new bit: the
-    stage's worst case).  Timed with CUDA events around the call; the library's stage events
-    give the Bloom (K3-K6) time.  Algorithmic traffic per probe = one 32-B sector read + one
-    32-B sector write-back; B200 moves a whole 128-B line per random access, which
-    the measured random-access peak (tools/micro/rand_sector.cu) reflects."""
-    cfg = CONFIGS["C5"]
-    n = args.hbm_docs
-    off, tok = gen_range(cfg, 0, n)
-    d_off = torch.from_numpy(off.view(np.int64)).to(dev)
-    d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
-    res = hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, "bloom")
-    # the blocked variant (SURVEY §8f NEXT #4): one 128-B line per (document, band)
-    res["blocked_variant"] = hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, "blocked")
-    del d_off, d_tok
-    torch.cuda.empty_cache()
-    return res
-
-
-def hbm_traffic(index, probes):
-    """DRAM bytes per step (read + write) of the standard filter's Bloom stage from the committed
-    ncu capture (profiles/bloom_hbm_traffic_C5.json, per probe x probes per step): a random probe
-    moves a whole 128-B line for K3's read and again for K4's atomic."""
-    if index != "bloom":
-        return None
+def load_json(name):
     try:
-        with open(os.path.join(ROOT, "profiles", "bloom_hbm_traffic_C5.json")) as f:
-            return json.load(f)["dram_bytes_per_probe"] * probes
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
     except Exception:
         return None
 
 
-def hbm_run(args, torch, dev, peaks, peak_src, cfg, d_off, d_tok, index):
-    from paper_2411_04257_b200 import LSHBloom
-    n = d_off.numel() - 1
-    eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=dev.index, index=index)
+def bloom_alone(torch, dev, make_engine, bhs, probes, peaks, peak_src, steps):
+    """The Bloom stage by itself (lshbloom_query_insert_bands: binning + window sweep + verdict,
+    or the random-access kernels, whichever the library picks) on freshly zeroed filters, one
+    batch of band hashes per step (bhs[0] warms up).  CUDA events on the launching stream around
+    each call.  Algorithmic traffic per probe = one 32-B sector read + one 32-B write-back
+    (SURVEY §8d), against the measured HBM copy peak."""
+    eng = make_engine()
     stream = torch.cuda.current_stream(dev)
-    steps, warm = max(3, min(args.steps, 10)), 2
-    tot = 0.0
-    for i in range(warm + steps):
+    ms = []
+    for i in range(steps + 1):
         eng.reset()
-        if i == warm:
-            eng.stage_times(enable=True)
         torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        eng.stage_times(enable=True)
         e0.record(stream)
-        flags = eng.query_insert(d_off, d_tok)
+        eng.query_insert_bands(bhs[i % len(bhs)])
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        if i >= warm:
-            tot += e0.elapsed_time(e1)
-    (k1_ms, bl_ms), (k1_n, bl_n) = eng.stage_times(enable=False)
+        st, _ = eng.stage_times(enable=False, all_stages=True)
+        if i:
+            ms.append((e0.elapsed_time(e1), st[2]))
     info = eng.info()
-    probes = n * cfg.b * eng.k
-    bl_step = bl_ms / max(1, bl_n)
-    # standard: a 32-B sector read + write-back per probe; blocked: one 128-B line read +
-    # write-back per (document, band), i.e. 256 / k bytes per probe
-    bpp = 64.0 if index == "bloom" else 256.0 / eng.k
-    alg_bytes = probes * bpp
+    eng.close()
+    t = statistics.median(m for m, _ in ms)
+    sweep_ms = statistics.median(x for _, x in ms)
     peak = float(peaks.get("hbm_gbs", 6546.0))
-    res = {"bound": "hbm", "index": index,
-           "workload": "C5 geometry (128 perms, b=20 r=6, n_expected=1e9, %.1f GB filters), "
-                       "first %d C5 documents per step, fresh filters" % (info["filter_bytes"] / 1e9, n),
-           "docs_per_s": n * steps / (tot / 1e3), "ms_per_step": tot / steps,
-           "bloom_ms_per_step": bl_step, "probes_per_step": probes,
-           "Gprobe_per_s": probes / bl_step / 1e6,
-           "achieved": alg_bytes / bl_step / 1e6, "peak": peak, "unit": "GB/s", "frac": alg_bytes / bl_step / 1e6 / peak,
-           "peak_source": "%s hbm_gbs" % peak_src,
-           "bytes_per_probe_algorithmic": round(bpp, 3),
-           "traffic": hbm_traffic(index, probes),
-           "dup_frac": float(flags.float().mean().item())}
+    alg = probes * 64.0
+    return {"bound": "hbm", "achieved": alg / t / 1e6, "peak": peak, "unit": "GB/s", "frac": alg / t / 1e6 / peak,
+            "ms_per_batch": t, "sweep_kernels_ms": sweep_ms, "probes": probes, "Gprobe_per_s": probes / t / 1e6,
+            "bytes_per_probe_algorithmic": 64, "path": "sweep" if info["sweeps"] else "random",
+            "filter_bytes": info["filter_bytes"], "peak_source": "%s hbm_gbs (copy)" % peak_src}
+
+
+def c5_leg(args, torch, dev, peaks, peak_src):
+    """C5 geometry (128 perms, b=20 r=6, n_expected=1e9 -> 20 x 3.0 GB filters, m > 2^32), 4M-
+    document stream batches: (a) the fused lshbloom_query_insert per batch (device-resident CSR,
+    filters zeroed between steps outside the timed call), (b) the Bloom stage alone on fresh
+    band hashes of the same documents under other hash seeds."""
+    from paper_2411_04257_b200 import LSHBloom
+    cfg = CONFIGS["C5"]
+    n = args.hbm_docs
+    off, tok = gen_range_parallel(cfg, 0, n)
+    d_off = torch.from_numpy(off.view(np.int64)).to(dev)
+    d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
+    steps = max(3, min(args.steps, 6))
+    stream = torch.cuda.current_stream(dev)
+    eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=dev.index)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    times, stages = [], []
+    for i in range(2 + steps):
+        eng.reset()
+        torch.cuda.synchronize(dev)
+        eng.stage_times(enable=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.query_insert(d_off, d_tok, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        st, _ = eng.stage_times(enable=False, all_stages=True)
+        if i >= 2:
+            times.append(e0.elapsed_time(e1))
+            stages.append(st)
+    fused_ms = statistics.median(times)
+    dup_frac = float(out.float().mean().item())
+    info = eng.info()
     eng.close()
     del eng
+    bhs = []
+    for s in range(3):
+        h = LSHBloom(cfg.num_perm, cfg.b, cfg.r, n, cfg.fp_rate, cfg.seed + 1000 + s, device=dev.index)
+        bhs.append(h.band_hashes(d_off, d_tok))
+        h.close()
+    del d_off, d_tok
+    torch.cuda.empty_cache()
+    probes = n * cfg.b * info["k"]
+    alone = bloom_alone(torch, dev, lambda: LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed,
+                                                     device=dev.index), bhs, probes, peaks, peak_src, steps)
+    tr = load_json("bloom_sweep_traffic_C5.json")
+    alone["traffic"] = tr["dram_bytes_per_probe"] * probes if tr else None
+    del bhs
+    torch.cuda.empty_cache()
+    return {"workload": "C5 geometry: 128 perms, b=20 r=6, n_expected=1e9 (%.1f GB of filters, m=%d > 2^32), "
+                        "%d-document stream batches" % (info["filter_bytes"] / 1e9, info["m"], n),
+            "fused_step": {"docs_per_s": n / (fused_ms / 1e3), "ms_per_batch": fused_ms,
+                           "stages_ms": {"minhash_k1": statistics.median(x[0] for x in stages),
+                                         "bloom_stage_span": statistics.median(x[1] for x in stages),
+                                         "sweep_kernels": statistics.median(x[2] for x in stages)},
+                           "dup_frac": dup_frac, "timing": "CUDA events around each query_insert call; "
+                                                           "filters zeroed between calls, untimed"},
+            "bloom_alone": alone}
+
+
+def secondary_c2(args, torch, dev, peaks):
+    """C2 (1M abstract-like documents per step, 128 perms, b16 r8, n_expected = 1M: 48 MB of
+    L2-resident filters): the fused step, device-resident, filters zeroed inside each step."""
+    from paper_2411_04257_b200 import LSHBloom
+    cfg = CONFIGS["C2"]
+    n = DOCS_PER_STEP["C2"]
+    off, tok = gen_range_parallel(cfg, 0, n)
+    d_off = torch.from_numpy(off.view(np.int64)).to(dev)
+    d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
+    eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=dev.index)
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    steps = max(5, min(args.steps, 20))
+    for _ in range(3):
+        eng.reset()
+        eng.query_insert(d_off, d_tok, out=out)
+    torch.cuda.synchronize(dev)
+    eng.stage_times(enable=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        eng.reset()
+        eng.query_insert(d_off, d_tok, out=out)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    (k1_ms, _), (k1_n, _) = eng.stage_times(enable=False)
+    ms = e0.elapsed_time(e1) / steps
+    evals = minhash_evals(off, cfg.num_perm, cfg.shingle_n)
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    ach = evals[0] / (k1_ms / max(1, k1_n) / 1e3)
+    res = {"workload": "C2: 1M abstract-like docs per step, 128 perms, b16 r8, n_expected 1M (%.0f MB of filters)"
+                       % (eng.info()["filter_bytes"] / 1e6),
+           "docs_per_s": n / (ms / 1e3), "ms_per_step": ms, "dup_frac": float(out.float().mean().item()),
+           "k1_roofline": {"achieved": ach / 1e9, "peak": k1_peak(evals, f_max) / 1e9, "unit": "Geval/s",
+                           "frac": ach / k1_peak(evals, f_max), "ms_per_launch": k1_ms / max(1, k1_n)}}
+    eng.close()
+    del d_off, d_tok
     torch.cuda.empty_cache()
     return res
 
@@ -325,7 +413,7 @@ def main():
     csum = checksum(off, tok)
     d_off = torch.from_numpy(off.view(np.int64)).to(dev)
     d_tok = torch.from_numpy(tok.view(np.int32)).to(dev)
-    evals = minhash_evals(off, cfg.num_perm, cfg.shingle_n)
+    evals = minhash_evals(off, cfg.num_perm, cfg.shingle_n)   # (total, exact-kernel, screened-kernel)
 
     if world > 1:
         sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, args.n_expected, cfg.fp_rate, cfg.seed,
@@ -445,39 +533,53 @@ def main():
     # ---- roofline of the dominant kernel (K1: shingles + MinHash + band hashes)
     peaks, peak_src = load_peaks()
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    # 4 IMAD.WIDE.U32 per (a x + b) mod P evaluation (two 61-bit operands -> four 32x32->64
-    # partial products); IMAD.WIDE issues at 0.25 warp-inst/clk/SMSP on sm_100a (fmaheavy,
-    # tools/micro/pipe_micro.cu) -> 2 evaluations / clk / SMSP.
-    peak_evals = 2.0 * 148 * 4 * f_max
+    peak_evals = k1_peak(evals, f_max)
     k1_per_launch_ms = k1_ms / max(1, k1_n)
-    achieved = evals / (k1_per_launch_ms / 1e3) if k1_n else None
+    achieved = evals[0] / (k1_per_launch_ms / 1e3) if k1_n else None
     roofline = {"bound": "alu", "achieved": achieved / 1e9 if achieved else None,
                 "peak": peak_evals / 1e9, "unit": "Geval/s",
                 "frac": (achieved / peak_evals) if achieved else None,
                 "traffic": load_traffic(args.config),
                 "kernel": "k1_minhash (fingerprints + MinHash + band hashes)",
-                "peak_source": "%s sm_max_mhz %.0f x 148 SMs x 4 SMSP x 2 evals/clk (fmaheavy IMAD.WIDE bound)"
-                               % (peak_src, f_max / 1e6),
-                "evals_per_launch": evals, "ms_per_launch": k1_per_launch_ms,
+                "peak_source": "%s sm_max_mhz %.0f x 148 SMs x 4 SMSP x evaluations/clk/SMSP of the kernel each "
+                               "document runs on (exact: 2 = four IMAD.WIDE at 1/4 rate; screened, >= 1024 "
+                               "shingles with 256 permutations: 8/3 = two IMAD.WIDE + two IMAD), weighted by "
+                               "evaluations" % (peak_src, f_max / 1e6),
+                "evals_per_launch": evals[0], "evals_exact_kernel": evals[1], "evals_screened_kernel": evals[2],
+                "ms_per_launch": k1_per_launch_ms,
                 "share_of_step": (k1_ms / max(1, args.steps)) / (ms / args.steps)}
 
     # K1 alone (lshbloom_band_hashes: one launch over the batch, the whole GPU, no Bloom
     # kernels beside it) -- the kernel's own rate, next to its rate inside the overlapped step
+    roofline_bloom = None
     if world == 1:
-        eng.band_hashes(d_off, d_tok)
+        bh_step = eng.band_hashes(d_off, d_tok)
         eng.stage_times(enable=True)
         for _ in range(3):
             eng.band_hashes(d_off, d_tok)
         (a_ms, _), (a_n, _) = eng.stage_times(enable=False)
         if a_n:
             roofline["alone_ms_per_launch"] = a_ms / a_n
-            roofline["alone_achieved"] = evals / (a_ms / a_n / 1e3) / 1e9
+            roofline["alone_achieved"] = evals[0] / (a_ms / a_n / 1e3) / 1e9
             roofline["alone_frac"] = roofline["alone_achieved"] / roofline["peak"]
+        # the headline config's Bloom stage by itself (same band hashes, filters zeroed per step)
+        if args.index != "classic":
+            probes = args.docs * cfg.b * eng.k
+            roofline_bloom = bloom_alone(
+                torch, dev, lambda: LSHBloom(cfg.num_perm, cfg.b, cfg.r, args.n_expected, cfg.fp_rate, cfg.seed,
+                                             device=local, index=args.index), [bh_step], probes, peaks, peak_src,
+                max(3, min(args.steps, 10)))
+        del bh_step
+
+    secondary = {}
+    if world == 1 and not args.no_secondary and args.config != "C2":
+        secondary["C2"] = secondary_c2(args, torch, dev, peaks)
 
     bloom_hbm = None
     if not args.no_hbm and world == 1:
         del flags
-        bloom_hbm = hbm_leg(args, torch, dev, peaks, peak_src)
+        torch.cuda.empty_cache()
+        bloom_hbm = c5_leg(args, torch, dev, peaks, peak_src)
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -506,9 +608,13 @@ def main():
                    "sub_batch": args.sub_batch or 32768, "csr_checksum_rank0": csum,
                    "dup_frac": dup_frac, "gen_s": round(gen_s, 1)},
         "roofline": roofline,
+        "roofline_bloom": roofline_bloom,
         "roofline_bloom_hbm": bloom_hbm,
+        "secondary": secondary,
         "step_wall_ms": device_step_wall,
-        "stages_ms_per_step": {"minhash_k1": k1_ms / max(1, args.steps), "bloom_k3_k6": bl_ms / max(1, args.steps)},
+        "stages_ms_per_step": {"minhash_k1": k1_ms / max(1, args.steps),
+                               "bloom_stage_span": bl_ms / max(1, args.steps),
+                               "note": "the Bloom stage runs on its own stream beside K1 (span, not busy time)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -83,7 +83,7 @@ struct lshbloom {
   // window-sweep Bloom stage (lb_sweep.cu)
   uint32_t bloom_path = 0;        // LSHBLOOM_PATH_AUTO / _RANDOM / _SWEEP
   uint32_t sweep_wb_force = 0, sweep_cap_force = 0;
-  DevBuf sw_cursor, sw_cursor2, sw_start, sw_rec, sw_miss, sw_eg;
+  DevBuf sw_cursor, sw_cursor2, sw_start, sw_rec, sw_miss, sw_eg, sw_ccursor, sw_crec, sw_bht;
   uint64_t sweeps = 0;            // sweeps run (lshbloom_info)
   // stage timing (lshbloom_stage_times): K1, Bloom stage, sweep kernels (K7x-K9)
   bool timing = false;
@@ -144,6 +144,7 @@ void free_all(lshbloom* h) {
   F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->tok[2].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
   F(h->sw_cursor.p); F(h->sw_cursor2.p); F(h->sw_start.p); F(h->sw_rec.p); F(h->sw_miss.p); F(h->sw_eg.p);
+  F(h->sw_ccursor.p); F(h->sw_crec.p); F(h->sw_bht.p);
   for (int i = 0; i < 3; i++) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
@@ -474,31 +475,65 @@ struct SweepPlan {
   bool use = false;
   uint32_t wb = 0, cap = 0;
   uint64_t nw = 0, nbins = 0, piece = 0;
+  bool two_level = false;         // K7a + K7b (k = 17)
+  uint32_t cb = 0, ccap = 0;
+  uint64_t ncb = 0;
 };
 
-// Window size and bin capacity for a batch of n documents (pieces of <= kSweepMaxDocs): the
-// largest window whose expected load mu = n k 2^wb / m stays <= 1536 records (so a bin of
-// mu + 7 sqrt(mu) + 64 fits the K8 CTA's 2048 register-held records), and whether the sweep
-// beats random access (AUTO: owned filters beyond 96 MB, i.e. not L2-resident, and >= 256
+// Bin capacity for an expected load of mu records: 7 standard deviations of a Poisson load, slack
+// for the band hashes near-duplicates share, and `pad` records of sector padding.
+// Rounded up to whole 32-byte sectors so that every bin starts sector-aligned.
+uint32_t sweep_cap_for(double mu, double pad = 0.0) {
+  return ((uint32_t)std::ceil(mu + 7.0 * std::sqrt(mu) + 64.0 + pad) + 3u) & ~3u;
+}
+
+// Window size and bin capacities for a batch of n documents (pieces of <= kSweepMaxDocs): the
+// largest window whose bin capacity (expected load mu = n k 2^wb / m, plus the sector padding
+// K7b adds per chunk) fits the K8 CTA's kSweepCapReg register-held records, the coarse buckets
+// of the two-level binning (<= kSweepMaxCoarse per band, <= 512 windows each), and whether the
+// sweep beats random access (AUTO: owned filters beyond 96 MB, i.e. not L2-resident, and >= 256
 // probes per 64 KB window).
 SweepPlan plan_sweep(const lshbloom* h, uint64_t n) {
   SweepPlan sp;
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC || h->bloom_path == LSHBLOOM_PATH_RANDOM || n == 0) return sp;
   sp.piece = std::min<uint64_t>(n, kSweepMaxDocs);
   const double rho = (double)sp.piece * h->k / (double)h->m;      // records per filter bit
+  const double tiles = std::ceil((double)sp.piece / kSweepTileDocs);
+  auto coarse = [&](uint32_t wb, uint32_t& cb, uint64_t& ncb, uint32_t& ccap) {
+    const uint64_t nw = (h->m + (1ull << wb) - 1) >> wb;
+    cb = 0;
+    while ((1u << cb) < kSweepMaxW && ((nw + (1ull << cb) - 1) >> cb) > kSweepMaxCoarse) cb++;
+    ncb = (nw + (1ull << cb) - 1) >> cb;
+    const double mu_c = rho * (double)(1ull << (wb + cb));
+    ccap = sweep_cap_for(mu_c, 3.0 * std::min(tiles, mu_c));
+    return ncb <= kSweepMaxCoarse;
+  };
+  // window bins: Poisson load + K7b's rounding of each window's tail to a whole sector; rounded
+  // to 16 records so that every bin starts on a 128-byte line (K7b writes whole lines)
+  auto fine_cap = [&](uint32_t wb, bool two) {
+    const double mu = rho * (double)(1ull << wb);
+    if (!two) return sweep_cap_for(mu);
+    return (sweep_cap_for(mu, 3.0) + 15u) & ~15u;
+  };
+  const bool two = h->k == 17;
   uint32_t wb = 10;
-  while (wb < 19 && rho * (double)(1ull << (wb + 1)) <= 1536.0) wb++;
+  while (wb < 19 && fine_cap(wb + 1, two) <= kSweepCapReg) wb++;
   if (h->sweep_wb_force) wb = h->sweep_wb_force;
   if (h->bloom_path == LSHBLOOM_PATH_AUTO) {
     const double fbytes = (double)h->bl * (double)h->W * 4.0;
-    if (!(fbytes > 96e6 && rho * 524288.0 >= 256.0 && rho * 1024.0 <= 1536.0)) return sp;
+    if (!(fbytes > 96e6 && rho * 524288.0 >= 256.0 && fine_cap(10, two) <= kSweepCapReg)) return sp;
   }
-  const double mu = rho * (double)(1ull << wb);
   sp.use = true;
   sp.wb = wb;
-  sp.cap = h->sweep_cap_force ? h->sweep_cap_force : (uint32_t)std::ceil(mu + 7.0 * std::sqrt(mu) + 64.0);
   sp.nw = (h->m + (1ull << wb) - 1) >> wb;
   sp.nbins = sp.nw * h->bl;
+  sp.two_level = two && coarse(wb, sp.cb, sp.ncb, sp.ccap);
+  if (getenv("LSHBLOOM_SWEEP_ONE_LEVEL")) sp.two_level = false;
+  sp.cap = h->sweep_cap_force ? h->sweep_cap_force : fine_cap(wb, sp.two_level);
+  if (sp.two_level && h->sweep_cap_force) {
+    sp.ccap = (std::max<uint32_t>(4, h->sweep_cap_force) + 3u) & ~3u;
+    sp.cap = (sp.cap + 15u) & ~15u;
+  }
   return sp;
 }
 
@@ -512,6 +547,10 @@ int ensure_zeroed(lshbloom* h, DevBuf& b, size_t bytes, cudaStream_t s) {
 
 int sweep_alloc(lshbloom* h, const SweepPlan& sp, cudaStream_t s) {
   const uint64_t recs = std::max<uint64_t>(sp.nbins * sp.cap, sp.piece * h->k * h->bl);
+  if (sp.two_level) {
+    LB_CUDA(h, ensure(h->sw_ccursor, h->bl * sp.ncb * 4));
+    LB_CUDA(h, ensure(h->sw_crec, h->bl * sp.ncb * sp.ccap * 8));
+  }
   LB_CUDA(h, ensure(h->sw_cursor, sp.nbins * 4));
   LB_CUDA(h, ensure(h->sw_cursor2, sp.nbins * 4));
   LB_CUDA(h, ensure(h->sw_start, (sp.nbins + 1) * 8));
@@ -539,12 +578,21 @@ SweepParams sweep_params(lshbloom* h, const SweepPlan& sp, const BloomParams& g,
   p.eg = (uint32_t*)h->sw_eg.p;
   p.i0 = (uint32_t)i0;
   p.n = (uint32_t)n;
+  p.two_level = sp.two_level ? 1 : 0;
+  if (sp.two_level) {
+    p.cb = sp.cb;
+    p.ncb = sp.ncb;
+    p.ccap = sp.ccap;
+    p.ccursor = (uint32_t*)h->sw_ccursor.p;
+    p.crec = (uint64_t*)h->sw_crec.p;
+  }
   return p;
 }
 
 int sweep_begin(lshbloom* h, const SweepParams& p, cudaStream_t s) {
   LB_CUDA(h, cudaMemsetAsync(p.cursor, 0, p.nbins * 4, s));
   LB_CUDA(h, cudaMemsetAsync(p.ovf, 0, 4, s));
+  if (p.two_level) LB_CUDA(h, cudaMemsetAsync(p.ccursor, 0, p.g.bl * p.ncb * 4, s));
   return LSHBLOOM_OK;
 }
 
@@ -569,6 +617,13 @@ int run_bloom_sweep(lshbloom* h, const SweepPlan& sp, const uint64_t* bh_dev, ui
                     uint64_t n, uint8_t* dup_dev, cudaStream_t s, const DupSink* peers) {
   int rc = sweep_alloc(h, sp, s);
   if (rc) return rc;
+  if (bh_si != 1 && h->bl > 1) {          // row-major [n][bl]: transpose so the binning reads coalesced
+    LB_CUDA(h, ensure(h->sw_bht, n * h->bl * 8));
+    h->launches += launch_transpose_bh(bh_dev, (uint64_t*)h->sw_bht.p, (uint32_t)n, h->bl, s);
+    bh_dev = (const uint64_t*)h->sw_bht.p;
+    bh_sj = n;
+    bh_si = 1;
+  }
   const BloomParams g = bloom_params(h, bh_dev, bh_sj, bh_si, dup_dev, peers);
   stage_begin(h, 1, s);
   for (uint64_t i0 = 0; i0 < n; i0 += kSweepMaxDocs) {

@@ -115,17 +115,26 @@ struct BloomParams {
 struct SweepParams {
   BloomParams g;             // geometry, seeds, filters, band hashes, dup sink, error gate
   uint32_t wb;               // log2 window bits (10..19)
-  uint32_t cap;              // records per bin in the fixed-capacity layout
+  uint32_t cap;              // records per window bin in the fixed-capacity layout
   uint64_t nw;               // windows per band = ceil(m / 2^wb)
   uint64_t nbins;            // bl * nw, band-major
-  uint32_t* cursor;          // [nbins] records binned (counts every record, including those beyond cap)
+  uint32_t* cursor;          // [nbins] records (+ sentinel padding) per window bin
   uint32_t* cursor2;         // [nbins] exact-layout scatter cursors
   uint64_t* start;           // [nbins + 1] exact layout: exclusive scan of cursor
   uint64_t* rec;             // records: fixed layout bin * cap + slot, exact layout start[bin] + slot
-  uint32_t* ovf;             // nonzero: some bin exceeded cap -> exact layout
+  uint32_t* ovf;             // nonzero: some bin exceeded its capacity -> exact layout
   uint64_t* miss;            // [n] bit jl set: band jl of sweep document d missed
-  uint32_t* eg;              // [grid][2^wb] earliest setter per position, for bins beyond 2048 records
+  uint32_t* eg;              // [grid][2^wb] earliest setter per position, for bins beyond kSweepCapReg
   uint32_t i0, n;            // this sweep = batch documents [i0, i0 + n)
+  // two-level binning (k = 17): K7a sorts each 512-document tile's records by coarse bucket
+  // (2^cb windows) in shared memory and writes them as runs; K7b re-sorts each coarse bucket by
+  // window in 4096-record chunks -- every record is written in coalesced runs, never scattered
+  uint32_t two_level;        // 1: K7a + K7b; 0: K7 writes records straight into window bins
+  uint32_t cb;               // log2 windows per coarse bucket
+  uint64_t ncb;              // coarse buckets per band = ceil(nw / 2^cb) (<= kSweepMaxCoarse)
+  uint32_t ccap;             // records (+ padding) per coarse bucket
+  uint32_t* ccursor;         // [bl * ncb]
+  uint64_t* crec;            // [bl * ncb * ccap]
 };
 
 struct ClassicParams {        // classic MinHashLSH index (lb_classic.cu)
@@ -155,8 +164,15 @@ int launch_classic(const ClassicParams& p, cudaStream_t s);
 int launch_sweep_bin(const SweepParams& p, uint32_t lo, uint32_t hi, cudaStream_t s);
 int launch_sweep_finish(const SweepParams& p, int grid, cudaStream_t s);
 int sweep_grid(int sm_count, uint32_t wb);     // K8 CTAs (persistent) for a window size
-constexpr int kSweepThreads = 512;               // K8 block size
+int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t bl, cudaStream_t s);
+constexpr int kSweepThreads = 256;               // K8 block size
 constexpr int kSweepRPT = 4;                     // records per thread held in registers
-constexpr uint32_t kSweepCapReg = kSweepThreads * kSweepRPT;   // 2048: larger bins take the global path
+constexpr uint32_t kSweepCapReg = kSweepThreads * kSweepRPT;   // 1024: larger bins take the global path
+constexpr uint32_t kSweepMaxCoarse = 1024;       // coarse buckets per band (K7a: one per thread)
+constexpr uint32_t kSweepTileDocs = 1024;        // K7a: documents per tile (= threads)
+constexpr uint32_t kSweepMaxW = 256;             // K7b: windows per coarse bucket (line staging each)
+constexpr uint32_t kSweepStage = 32;             // K7b: staged records per window (flushed in 16s)
+constexpr uint32_t kSweepBThreads = 512;         // K7b block size
+constexpr uint32_t kSweepChunk = 2048;           // K7b: records per chunk (4 per thread)
 
 }  // namespace lb

@@ -81,7 +81,7 @@ def test_exact_layout_after_overflow(c1, cap):
 
 
 @pytest.mark.parametrize("cap", [0, 2])
-def test_bins_beyond_2048_records(c1, cap):
+def test_bins_beyond_register_capacity(c1, cap):
     # m = 239,627 < 2^19: one window per band, ~170K records per bin -> the global-memory branch
     cfg, off, tok, bh, dup, ref = c1
     idx = sweep(cfg, sweep_window_log2=19, sweep_cap=cap)
