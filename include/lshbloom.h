@@ -29,8 +29,9 @@
  *    memory otherwise; pinned host memory enables overlapped copies).  The library owns
  *    filters, coefficients and scratch (cudaMalloc) and frees them in lshbloom_destroy.
  *  - A handle is not thread-safe.  query_insert calls are serialised by the caller and
- *    their order is the stream order.  Every call is complete (its stream
- *    synchronised) when it returns.
+ *    their order is the stream order.  Every call except
+ *    lshbloom_query_insert_async (and lshbloom_reset while async batches are in flight) is
+ *    complete when it returns.
  *  - Outputs are pure functions of (parameters, seed, ordered concatenation of batches):
  *    independent of batch boundaries, GPU count and launch configuration.
  */
@@ -201,6 +202,23 @@ LSHBLOOM_API int lshbloom_band_hashes_sharded(lshbloom *h, const lshbloom_batch 
  * ranks; see lshbloom_query_insert_bands and paper_2411_04257_b200.sharded). */
 LSHBLOOM_API int lshbloom_query_insert(lshbloom *h, const lshbloom_batch *batch, uint8_t *dup_out);
 
+/* Asynchronous form of lshbloom_query_insert, for streams of batches (the index is a
+ * stream; S:427 serial order).  Enqueues the batch and returns without waiting: the batch's
+ * MinHash kernels run while the previous batch's Bloom stage is still working, and Bloom stages
+ * run in call order, so the flags are exactly those of the synchronous calls in the same order.
+ * At most two batches are in flight; a third call first waits for the oldest.  dup_out, and for
+ * host batches the offsets / tokens (pinned memory, or the copies serialise), must stay valid
+ * and unmodified until lshbloom_sync returns.  Host-checkable errors (NULL pointers, offsets[0],
+ * chunk bounds) are returned at once; the device-side verdict on the CSR (malformed offsets,
+ * empty document) is returned by lshbloom_sync -- a rejected batch inserts nothing, later
+ * batches are processed normally.  Other entry points wait for the batches in flight first;
+ * lshbloom_reset does not (it is ordered on the device between the batches around it). */
+LSHBLOOM_API int lshbloom_query_insert_async(lshbloom *h, const lshbloom_batch *batch, uint8_t *dup_out);
+
+/* Wait for every batch enqueued with lshbloom_query_insert_async; returns the first device-side
+ * error among them (1 or 2, lshbloom_last_error names it) or 0, and clears it. */
+LSHBLOOM_API int lshbloom_sync(lshbloom *h);
+
 /* Bloom stage only, for band-sharded use: bh_owned[n_docs][band_hi-band_lo] holds the
  * band hashes of the owned bands for n_docs documents in global stream order;
  * hit_out[n_docs] = OR over the owned bands of the per-band verdicts.  Pointers are device
@@ -231,7 +249,9 @@ LSHBLOOM_API int lshbloom_band_hashes_to_peers(lshbloom *h, const lshbloom_batch
 LSHBLOOM_API int lshbloom_query_insert_bands_peers(lshbloom *h, const uint64_t *bh_owned, uint64_t n_global,
                                                    const uint64_t *doc_start, void *const *peer_flags, void *stream);
 
-/* Zero every owned filter and the document count (as right after create). */
+/* Zero every owned filter and the document count (as right after create).  Ordered on the device
+ * after the batches already enqueued and before later ones; waits for completion unless async
+ * batches are in flight. */
 LSHBLOOM_API int lshbloom_reset(lshbloom *h);
 
 /* Copy owned band (band_hi > j >= band_lo, global index j) filter words to host memory

@@ -64,7 +64,8 @@ EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloo
            "lshbloom_query_insert_bands", "lshbloom_reset", "lshbloom_filter_copy", "lshbloom_info",
            "lshbloom_stage_times", "lshbloom_save", "lshbloom_load", "lshbloom_last_error",
            "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan",
-           "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers")
+           "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers", "lshbloom_query_insert_async",
+           "lshbloom_sync")
 
 
 def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
@@ -78,8 +79,9 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     lib.lshbloom_destroy.argtypes = [vp]
     lib.lshbloom_destroy.restype = None
     for f in ("lshbloom_signatures", "lshbloom_band_hashes", "lshbloom_band_hashes_sharded",
-              "lshbloom_query_insert"):
+              "lshbloom_query_insert", "lshbloom_query_insert_async"):
         getattr(lib, f).argtypes = [vp, ctypes.POINTER(_Batch), vp]
+    lib.lshbloom_sync.argtypes = [vp]
     lib.lshbloom_query_insert_bands.argtypes = [vp, vp, u64, i32, vp, vp]
     lib.lshbloom_reset.argtypes = [vp]
     lib.lshbloom_filter_copy.argtypes = [vp, u32, vp]
@@ -98,7 +100,8 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     lib.lshbloom_launch_count.restype = u64
     for f in EXPORTS:
         if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan",
-           "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers"):
+           "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers", "lshbloom_query_insert_async",
+           "lshbloom_sync"):
             getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -277,6 +280,26 @@ class LSHBloom:
             _check_out(out, n, 1, dev)
         self._check(self._lib.lshbloom_query_insert(self._h, ctypes.byref(bt), self._ptr(out)))
         return out
+
+    def query_insert_async(self, offsets, tokens, *, out=None, stream=None):
+        """Enqueue a batch (lshbloom_query_insert_async): returns its flag buffer at once; the
+        flags are valid after sync().  The inputs and the returned buffer are kept alive until
+        then."""
+        bt, keep, n, dev = self._batch(offsets, tokens, stream)
+        if out is None:
+            out = self._out((n,), np.uint8, _torch_dtype("uint8"), dev, offsets)
+        else:
+            _check_out(out, n, 1, dev)
+        self._check(self._lib.lshbloom_query_insert_async(self._h, ctypes.byref(bt), self._ptr(out)))
+        self._inflight = (getattr(self, "_inflight", []) + [(keep, out)])[-2:]
+        return out
+
+    def sync(self):
+        """Wait for the async batches; raises the first device-side error among them."""
+        try:
+            self._check(self._lib.lshbloom_sync(self._h))
+        finally:
+            self._inflight = []
 
     def query_insert_bands(self, bh_owned, *, out=None, stream=None):
         """Bloom stage only: bh_owned [n][band_hi-band_lo] -> hit flags [n] (OR over owned bands)."""

@@ -73,8 +73,24 @@ struct lshbloom {
   uint64_t* d_clist = nullptr;    // contested probes of a sub-batch (sub_batch * bl * k)
   uint32_t* d_cb = nullptr;       // contested-position summary bits (2^cb_log2)
   uint32_t cb_log2 = 26;            // 8 MB: ~0.2 % of first arrivals collide with a contested position
-  ErrState* d_err = nullptr;
+  ErrState* d_err_base = nullptr; // [0]: synchronous calls; [1 + slot]: async query_insert batches
+  ErrState* d_err = nullptr;      // the state of the call being enqueued
   DevBuf off, tok[3], bh, dup, sig, part;   // tok: host-batch staging buffers
+  // query_insert batches in flight (lshbloom_query_insert_async / lshbloom_sync): at most two,
+  // each with its own band-hash, offsets and flag buffers and error state, so that batch t+1's K1
+  // runs while batch t's Bloom stage is still working (the Bloom stream keeps them in order)
+  struct Slot {
+    bool busy = false;
+    uint64_t n = 0, seq = 0;
+    cudaEvent_t done = nullptr;
+    DevBuf bh, off, dup;
+  } slot[2];
+  int next_slot = 0;
+  uint64_t seq = 0;
+  int async_rc = 0;               // first error of a completed async batch, until lshbloom_sync
+  std::string async_msg;
+  cudaStream_t k1_stream1 = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_pre = nullptr;
   uint64_t doc_count = 0, launches = 0;
   // classic MinHashLSH index (index_kind = LSHBLOOM_INDEX_CLASSIC)
   uint64_t* d_ckeys = nullptr;    // [bl][2^c_log2cap]
@@ -87,8 +103,9 @@ struct lshbloom {
   uint64_t sweeps = 0;            // sweeps run (lshbloom_info)
   // stage timing (lshbloom_stage_times): K1, Bloom stage, sweep kernels (K7x-K9)
   bool timing = false;
-  cudaEvent_t tev[2 * LSHBLOOM_NSTAGES] = {};
-  bool pend[LSHBLOOM_NSTAGES] = {};
+  int tset = 0;                   // event set of the call being enqueued: 0, 1 (async slots), 2 (sync)
+  cudaEvent_t tev[3][2 * LSHBLOOM_NSTAGES] = {};
+  bool pend[3][LSHBLOOM_NSTAGES] = {};
   double stage_ms[LSHBLOOM_NSTAGES] = {};
   uint64_t stage_n[LSHBLOOM_NSTAGES] = {};
   std::string err;
@@ -141,7 +158,14 @@ int check_handle(lshbloom* h) {
 void free_all(lshbloom* h) {
   auto F = [](void* p) { if (p) cudaFree(p); };
   F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_clist); F(h->d_cb); F(h->d_ekey);
-  F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err);
+  F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err_base);
+  for (auto& sl : h->slot) {
+    F(sl.bh.p); F(sl.off.p); F(sl.dup.p);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
+  if (h->k1_stream1) cudaStreamDestroy(h->k1_stream1);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_pre) cudaEventDestroy(h->ev_pre);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->tok[2].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
   F(h->sw_cursor.p); F(h->sw_cursor2.p); F(h->sw_start.p); F(h->sw_rec.p); F(h->sw_miss.p); F(h->sw_eg.p);
   F(h->sw_ccursor.p); F(h->sw_crec.p); F(h->sw_bht.p);
@@ -149,8 +173,9 @@ void free_all(lshbloom* h) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
   }
-  for (int i = 0; i < 2 * LSHBLOOM_NSTAGES; i++)
-    if (h->tev[i]) cudaEventDestroy(h->tev[i]);
+  for (auto& set : h->tev)
+    for (auto& e : set)
+      if (e) cudaEventDestroy(e);
   if (h->ev_fuse) cudaEventDestroy(h->ev_fuse);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->k1_stream2) cudaStreamDestroy(h->k1_stream2);
@@ -179,25 +204,64 @@ int check_batch(lshbloom* h, const lshbloom_batch* b) {
 }
 
 void stage_begin(lshbloom* h, int st, cudaStream_t s) {
-  if (h->timing) cudaEventRecord(h->tev[2 * st], s);
+  if (h->timing) cudaEventRecord(h->tev[h->tset][2 * st], s);
 }
 void stage_end(lshbloom* h, int st, cudaStream_t s) {
   if (h->timing) {
-    cudaEventRecord(h->tev[2 * st + 1], s);
-    h->pend[st] = true;
+    cudaEventRecord(h->tev[h->tset][2 * st + 1], s);
+    h->pend[h->tset][st] = true;
   }
 }
-// after the stream is synchronised
-void stage_collect(lshbloom* h) {
+// after the work of event set `set` is complete
+void stage_collect(lshbloom* h, int set = 2) {
   for (int st = 0; st < LSHBLOOM_NSTAGES; st++) {
-    if (!h->pend[st]) continue;
+    if (!h->pend[set][st]) continue;
     float ms = 0;
-    if (cudaEventElapsedTime(&ms, h->tev[2 * st], h->tev[2 * st + 1]) == cudaSuccess) {
+    if (cudaEventElapsedTime(&ms, h->tev[set][2 * st], h->tev[set][2 * st + 1]) == cudaSuccess) {
       h->stage_ms[st] += ms;
       h->stage_n[st] += 1;
     }
-    h->pend[st] = false;
+    h->pend[set][st] = false;
   }
+}
+
+// Host-side completion of an async batch: its error state (offsets / empty document, the
+// device-side K0 verdict) becomes the pending async result; a rejected batch inserted nothing.
+int collect(lshbloom* h, int si) {
+  lshbloom::Slot& sl = h->slot[si];
+  if (!sl.busy) return LSHBLOOM_OK;
+  LB_CUDA(h, cudaEventSynchronize(sl.done));
+  sl.busy = false;
+  stage_collect(h, si);
+  ErrState e;
+  LB_CUDA(h, cudaMemcpy(&e, h->d_err_base + 1 + si, sizeof e, cudaMemcpyDeviceToHost));
+  if (e.flags || e.first_empty != ~0ull) {
+    h->doc_count -= std::min(h->doc_count, sl.n);
+    if (!h->async_rc) {
+      h->async_rc = e.flags ? LSHBLOOM_EUSAGE : LSHBLOOM_EDATA;
+      h->async_msg = e.flags ? "malformed offsets (offsets[0] != 0 or decreasing)"
+                             : "empty document at index " + std::to_string(e.first_empty);
+    }
+  }
+  return LSHBLOOM_OK;
+}
+
+// Wait for every batch in flight, oldest first.
+int drain(lshbloom* h) {
+  const int first = h->slot[0].busy && h->slot[1].busy ? (h->slot[0].seq < h->slot[1].seq ? 0 : 1)
+                                                       : (h->slot[0].busy ? 0 : 1);
+  int rc = collect(h, first);
+  if (!rc) rc = collect(h, first ^ 1);
+  return rc;
+}
+
+// ensure() for scratch shared by the batches in flight: growing it first drains them.
+int grow(lshbloom* h, DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return LSHBLOOM_OK;
+  int rc = drain(h);
+  if (rc) return rc;
+  LB_CUDA(h, ensure(b, bytes));
+  return LSHBLOOM_OK;
 }
 
 // Owner-major layout for the band-sharded all-to-all (lshbloom_band_hashes_sharded).
@@ -547,18 +611,16 @@ int ensure_zeroed(lshbloom* h, DevBuf& b, size_t bytes, cudaStream_t s) {
 
 int sweep_alloc(lshbloom* h, const SweepPlan& sp, cudaStream_t s) {
   const uint64_t recs = std::max<uint64_t>(sp.nbins * sp.cap, sp.piece * h->k * h->bl);
-  if (sp.two_level) {
-    LB_CUDA(h, ensure(h->sw_ccursor, h->bl * sp.ncb * 4));
-    LB_CUDA(h, ensure(h->sw_crec, h->bl * sp.ncb * sp.ccap * 8));
-  }
-  LB_CUDA(h, ensure(h->sw_cursor, sp.nbins * 4));
-  LB_CUDA(h, ensure(h->sw_cursor2, sp.nbins * 4));
-  LB_CUDA(h, ensure(h->sw_start, (sp.nbins + 1) * 8));
-  LB_CUDA(h, ensure(h->sw_rec, recs * 8));
-  int rc = ensure_zeroed(h, h->sw_miss, sp.piece * 8, s);
-  if (rc) return rc;
-  LB_CUDA(h, ensure(h->sw_eg, (size_t)sweep_grid(h->sm_count, sp.wb) << sp.wb << 2));
-  return LSHBLOOM_OK;
+  int rc = 0;
+  if (sp.two_level &&
+      ((rc = grow(h, h->sw_ccursor, h->bl * sp.ncb * 4)) || (rc = grow(h, h->sw_crec, h->bl * sp.ncb * sp.ccap * 8))))
+    return rc;
+  if ((rc = grow(h, h->sw_cursor, sp.nbins * 4)) || (rc = grow(h, h->sw_cursor2, sp.nbins * 4)) ||
+      (rc = grow(h, h->sw_start, (sp.nbins + 1) * 8)) || (rc = grow(h, h->sw_rec, recs * 8)) ||
+      (rc = grow(h, h->sw_eg, (size_t)sweep_grid(h->sm_count, sp.wb) << sp.wb << 2)))
+    return rc;
+  if (sp.piece * 8 > h->sw_miss.cap && (rc = drain(h))) return rc;
+  return ensure_zeroed(h, h->sw_miss, sp.piece * 8, s);
 }
 
 SweepParams sweep_params(lshbloom* h, const SweepPlan& sp, const BloomParams& g, uint64_t i0, uint64_t n) {
@@ -693,12 +755,24 @@ uint64_t fuse_chunk_end(uint64_t d0, uint64_t n, uint32_t npl) {
   return d0 + kFuseDocs;
 }
 
-int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8_t* ddup) {
+// Enqueue one query_insert batch into slot `si` (its buffers and error state) without waiting for
+// it: K1 chunks on the handle's K1 streams, the Bloom stage on the Bloom stream (stream order =
+// batch order, which is all the exact semantics need), the flags copied out (host batches) and
+// the slot's `done` event recorded on the Bloom stream.  The caller's stream s only provides the
+// inputs: the K1 streams wait for its current position; nothing on s waits for this batch.
+// ddup: device flag buffer (the caller's when on_device, else the slot's); dup_host: host flags.
+int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int si, uint8_t* ddup, uint8_t* dup_host) {
   const uint64_t n = b->n_docs;
-  uint64_t* bh = (uint64_t*)h->bh.p;
+  lshbloom::Slot& sl = h->slot[si];
+  h->d_err = h->d_err_base + 1 + si;
+  h->tset = si;
+  LB_CUDA(h, ensure(sl.bh, n * h->bl * sizeof(uint64_t)));
+  uint64_t* bh = (uint64_t*)sl.bh.p;
   MinhashParams p = base_params(h);
-  if (h->npl >= 8)   // scratch of the length-partitioned K1 launches (lb_minhash.cu), per K1 stream
-    LB_CUDA(h, ensure(h->part, (6 * (size_t)b->n_docs + 6) * sizeof(uint32_t)));
+  if (h->npl >= 8) {   // scratch of the length-partitioned K1 launches (lb_minhash.cu), per K1 stream
+    int rc0 = grow(h, h->part, (6 * (size_t)b->n_docs + 6) * sizeof(uint32_t));
+    if (rc0) return rc0;
+  }
   p.bh_out = bh;
   p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
   const uint64_t chunk_tokens = b->on_device ? 0 : kChunkTokens;
@@ -748,39 +822,46 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
       d0 = d1;
     }
   }
-  int rc = reset_err(h, s);
-  if (rc) return rc;
-  if (sp.use && (rc = sweep_alloc(h, sp, s))) return rc;
+  int rc;
+  if (sp.use && (rc = sweep_alloc(h, sp, h->bloom_stream))) return rc;
   const BloomParams bp = bloom_params(h, bh, n, 1, ddup, nullptr);
+  // K1 chunks alternate between the K1 streams: each launch ends with a tail in which its last
+  // documents finish on a few warps, and the next chunk's blocks fill the SM slots meanwhile.
+  // Each stream has its own work counter, partition scratch and staging buffer (host batches).
+  const bool alt = h->k1_alt;
+  const int nks = alt ? h->k1_nstreams : 1;
+  cudaStream_t kst[3] = {h->k1_stream1, h->k1_stream2, h->k1_stream3};
+  cudaStream_t s0 = kst[0];
+  LB_CUDA(h, cudaEventRecord(h->ev_in, s));                // the inputs, as of this call
+  LB_CUDA(h, cudaStreamWaitEvent(s0, h->ev_in, 0));
+  if ((rc = reset_err(h, s0))) return rc;
   int nbuf = 2;
   if (b->on_device) {
-    h->launches += launch_validate(b->offsets, n, h->d_err, s);
+    h->launches += launch_validate(b->offsets, n, h->d_err, s0);
     p.offsets = b->offsets;
     p.tokens = b->tokens;
     p.tok_base = 0;
   } else {
     // No O(n) host pass: the offsets are validated on the device (K0), which gates every kernel;
     // the host only checked what its own copies depend on (offsets[0], chunk bounds, above).
-    LB_CUDA(h, ensure(h->off, (n + 1) * sizeof(uint64_t)));
-    LB_CUDA(h, cudaMemcpyAsync(h->off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    h->launches += launch_validate((const uint64_t*)h->off.p, n, h->d_err, s);
+    LB_CUDA(h, ensure(sl.off, (n + 1) * sizeof(uint64_t)));
+    LB_CUDA(h, cudaMemcpyAsync(sl.off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s0));
+    h->launches += launch_validate((const uint64_t*)sl.off.p, n, h->d_err, s0);
     nbuf = host_bufs(n, b->offsets[n]);
     const uint64_t buf_tokens = std::max<uint64_t>(1, std::min(chunk_tokens, b->offsets[n]));
-    for (int i = 0; i < nbuf; i++) LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
-    p.offsets = (const uint64_t*)h->off.p;
+    for (int i = 0; i < nbuf; i++)
+      if (buf_tokens * sizeof(uint32_t) > h->tok[i].cap) {
+        LB_CUDA(h, cudaEventSynchronize(h->ev_k1[i]));     // its last reader is done
+        LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
+      }
+    p.offsets = (const uint64_t*)sl.off.p;
   }
-  LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, s));
-  LB_CUDA(h, cudaEventRecord(h->ev_fuse, s));
-  LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
-  // K1 chunks alternate between s and k1_stream2: each launch ends with a tail in which its last
-  // documents finish on a few warps, and the next chunk's blocks fill the SM slots meanwhile.
-  // Each stream has its own work counter, partition scratch and staging buffer (host batches).
-  const bool alt = h->k1_alt;
-  const int nks = alt ? h->k1_nstreams : 1;
-  cudaStream_t kst[3] = {s, h->k1_stream2, h->k1_stream3};
-  for (int k = 1; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_fuse, 0));
+  LB_CUDA(h, cudaEventRecord(h->ev_pre, s0));               // error gate and offsets ready
+  for (int k = 1; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_pre, 0));
+  LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_pre, 0));
+  LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, h->bloom_stream));
   int c = 0;
-  stage_begin(h, 0, s);
+  stage_begin(h, 0, s0);
   for (const auto& ch : chunks) {
     const uint64_t d0 = ch.first, d1 = ch.second;
     if (!b->on_device) {
@@ -814,13 +895,13 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     LB_CUDA(h, cudaGetLastError());
     if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[c % nbuf], ks));
     LB_CUDA(h, cudaEventRecord(h->ev_fuse, ks));
-    if (d1 == n) {   // every K1 stream joined into s before the stage's end mark
+    if (d1 == n) {   // every K1 stream joined into the first before the stage's end mark
       cudaEvent_t ej[3] = {nullptr, h->ev_join, h->ev_join3};
       for (int k = 1; k < nks; k++) {
         LB_CUDA(h, cudaEventRecord(ej[k], kst[k]));
-        LB_CUDA(h, cudaStreamWaitEvent(s, ej[k], 0));
+        LB_CUDA(h, cudaStreamWaitEvent(s0, ej[k], 0));
       }
-      stage_end(h, 0, s);
+      stage_end(h, 0, s0);
     }
     LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
     if (!sp.use) {
@@ -836,16 +917,26 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint8
     }
     c++;
   }
-  LB_CUDA(h, cudaEventRecord(h->ev_fuse, h->bloom_stream));
-  LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_fuse, 0));
+  if (dup_host) LB_CUDA(h, cudaMemcpyAsync(dup_host, ddup, n, cudaMemcpyDeviceToHost, h->bloom_stream));
+  LB_CUDA(h, cudaEventRecord(sl.done, h->bloom_stream));
   return LSHBLOOM_OK;
 }
 
 int finish(lshbloom* h, cudaStream_t s) {
   LB_CUDA(h, cudaStreamSynchronize(s));
   LB_CUDA(h, cudaGetLastError());
-  stage_collect(h);
+  stage_collect(h, 2);
   return read_err(h);
+}
+
+// Synchronous entry points other than query_insert: drain the async batches first, then run on
+// error state 0 / event set 2.
+int begin_sync(lshbloom* h) {
+  int rc = drain(h);
+  if (rc) return rc;
+  h->d_err = h->d_err_base;
+  h->tset = 2;
+  return LSHBLOOM_OK;
 }
 
 }  // namespace
@@ -958,6 +1049,10 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaStreamCreateWithFlags(&h->k1_stream2, cudaStreamNonBlocking));
   CR(cudaStreamCreateWithFlags(&h->k1_stream3, cudaStreamNonBlocking));
   CR(cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming));
+  CR(cudaStreamCreateWithFlags(&h->k1_stream1, cudaStreamNonBlocking));
+  CR(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
+  CR(cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
+  for (auto& sl : h->slot) CR(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
   if (const char* e = getenv("LSHBLOOM_K1_STREAMS")) h->k1_nstreams = std::min(3, std::max(1, atoi(e)));
   if (const char* e = getenv("LSHBLOOM_K1_ALT")) h->k1_alt = atoi(e) != 0;
   h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
@@ -967,7 +1062,8 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     CR(cudaEventCreateWithFlags(&h->ev_k1[i], cudaEventDisableTiming));
     CR(cudaEventRecord(h->ev_k1[i], h->own_stream));
   }
-  for (int i = 0; i < 2 * LSHBLOOM_NSTAGES; i++) CR(cudaEventCreate(&h->tev[i]));
+  for (auto& set : h->tev)
+    for (auto& ev : set) CR(cudaEventCreate(&ev));
 
   // Hash family (DESIGN R5), in the kernel's limb layout.
   std::vector<PermCoef> coef(32 * npl);
@@ -1017,8 +1113,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     CR(cudaMemset(h->d_cvals, 0xFF, tbytes));   // no document yet
     CR(cudaMalloc(&h->d_counters, 16 * 4));
     CR(cudaMemset(h->d_counters, 0, 16 * 4));
-    CR(cudaMalloc(&h->d_err, sizeof(ErrState)));
-    CR(cudaMemset(h->d_err, 0, sizeof(ErrState)));
+    CR(cudaMalloc(&h->d_err_base, 3 * sizeof(ErrState)));
+    CR(cudaMemset(h->d_err_base, 0, 3 * sizeof(ErrState)));
+    h->d_err = h->d_err_base;
     CR(cudaDeviceSynchronize());
     *out = h;
     return LSHBLOOM_OK;
@@ -1048,8 +1145,9 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaMalloc(&h->d_cb, 1ull << (h->cb_log2 - 3)));
   CR(cudaMalloc(&h->d_counters, 16 * 4));
   CR(cudaMemset(h->d_counters, 0, 16 * 4));
-  CR(cudaMalloc(&h->d_err, sizeof(ErrState)));
-  CR(cudaMemset(h->d_err, 0, sizeof(ErrState)));
+  CR(cudaMalloc(&h->d_err_base, 3 * sizeof(ErrState)));
+  CR(cudaMemset(h->d_err_base, 0, 3 * sizeof(ErrState)));
+  h->d_err = h->d_err_base;
   CR(cudaDeviceSynchronize());
 #undef CR
   *out = h;
@@ -1060,7 +1158,7 @@ void lshbloom_destroy(lshbloom* h) {
   if (!h) return;
   {
     DeviceGuard g(h->device);
-    if (h->own_stream) cudaStreamSynchronize(h->own_stream);
+    cudaDeviceSynchronize();                 // batches in flight, every internal stream
     free_all(h);
   }
   delete h;
@@ -1071,6 +1169,7 @@ int lshbloom_signatures(lshbloom* h, const lshbloom_batch* b, uint32_t* sig_out)
   if (rc) return rc;
   if ((rc = check_batch(h, b))) return rc;
   if (!sig_out) return fail(h, LSHBLOOM_EUSAGE, "NULL sig_out");
+  if ((rc = begin_sync(h))) return rc;
   DeviceGuard g(h->device);
   cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
   const size_t bytes = b->n_docs * h->cfg.num_perm * sizeof(uint32_t);
@@ -1091,6 +1190,7 @@ static int band_hashes_impl(lshbloom* h, const lshbloom_batch* b, uint64_t* bh_o
   if (rc) return rc;
   if ((rc = check_batch(h, b))) return rc;
   if (!bh_out) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_out");
+  if ((rc = begin_sync(h))) return rc;
   DeviceGuard g(h->device);
   cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
   const size_t bytes = b->n_docs * h->cfg.b * sizeof(uint64_t);
@@ -1125,26 +1225,78 @@ int lshbloom_stage_times(lshbloom* h, int32_t enable, double* ms_out, uint64_t* 
   return LSHBLOOM_OK;
 }
 
-int lshbloom_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out) {
+// Shared by the synchronous and asynchronous forms: validate, take the next slot (waiting for
+// the batch that last used it), enqueue.
+static int enqueue_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out, int* slot_out) {
   int rc = check_handle(h);
   if (rc) return rc;
   if ((rc = check_batch(h, b))) return rc;
   if (!dup_out) return fail(h, LSHBLOOM_EUSAGE, "NULL dup_out");
-  if ((rc = classic_capacity(h, b->n_docs))) return rc;
+  if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) {
+    // the classic index keeps the document count in its table layout: no batches in flight
+    if ((rc = drain(h))) return rc;
+    if ((rc = classic_capacity(h, b->n_docs))) return rc;
+  }
   DeviceGuard g(h->device);
   cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
-  const uint64_t n = b->n_docs;
-  LB_CUDA(h, ensure(h->bh, n * h->bl * sizeof(uint64_t)));
+  const int si = h->next_slot;
+  if ((rc = collect(h, si))) return rc;                    // the batch two calls back is done
+  lshbloom::Slot& sl = h->slot[si];
   uint8_t* ddup = dup_out;
   if (!b->on_device) {
-    LB_CUDA(h, ensure(h->dup, n));
-    ddup = (uint8_t*)h->dup.p;
+    LB_CUDA(h, ensure(sl.dup, b->n_docs));
+    ddup = (uint8_t*)sl.dup.p;
   }
-  if ((rc = run_query_insert(h, b, s, ddup))) return rc;
-  if (!b->on_device) LB_CUDA(h, cudaMemcpyAsync(dup_out, ddup, n, cudaMemcpyDeviceToHost, s));
-  if ((rc = finish(h, s))) return rc;
-  h->doc_count += n;
+  if ((rc = run_query_insert(h, b, s, si, ddup, b->on_device ? nullptr : dup_out))) {
+    // nothing of this batch can have mutated the filters (its K0 gate or a host check failed
+    // before any launch), but kernels may be queued: let them finish before returning
+    cudaStreamSynchronize(h->bloom_stream);
+    return rc;
+  }
+  sl.busy = true;
+  sl.n = b->n_docs;
+  sl.seq = ++h->seq;
+  h->next_slot ^= 1;
+  h->doc_count += b->n_docs;
+  if (slot_out) *slot_out = si;
   return LSHBLOOM_OK;
+}
+
+int lshbloom_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if ((rc = drain(h))) return rc;
+  int si = 0;
+  if ((rc = enqueue_query_insert(h, b, dup_out, &si))) return rc;
+  DeviceGuard g(h->device);
+  cudaStream_t s = b->stream ? (cudaStream_t)b->stream : h->own_stream;
+  LB_CUDA(h, cudaStreamWaitEvent(s, h->slot[si].done, 0));  // stream order for the caller's later work
+  LB_CUDA(h, cudaGetLastError());
+  if ((rc = collect(h, si))) return rc;
+  rc = h->async_rc;
+  if (rc) {
+    h->err = h->async_msg;
+    h->async_rc = 0;
+  }
+  return rc;
+}
+
+int lshbloom_query_insert_async(lshbloom* h, const lshbloom_batch* b, uint8_t* dup_out) {
+  return enqueue_query_insert(h, b, dup_out, nullptr);
+}
+
+int lshbloom_sync(lshbloom* h) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  DeviceGuard g(h->device);
+  if ((rc = drain(h))) return rc;
+  LB_CUDA(h, cudaStreamSynchronize(h->bloom_stream));
+  rc = h->async_rc;
+  if (rc) {
+    h->err = h->async_msg;
+    h->async_rc = 0;
+  }
+  return rc;
 }
 
 int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t n_docs, int32_t on_device,
@@ -1153,6 +1305,7 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   if (rc) return rc;
   if (!bh_owned || !hit_out) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_owned / hit_out");
   if (n_docs == 0 || n_docs > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_docs must be in [1, 2^32)");
+  if ((rc = begin_sync(h))) return rc;
   if ((rc = classic_capacity(h, n_docs))) return rc;
   DeviceGuard g(h->device);
   cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
@@ -1181,6 +1334,7 @@ int lshbloom_band_hashes_to_peers(lshbloom* h, const lshbloom_batch* b, uint64_t
   if ((rc = check_batch(h, b))) return rc;
   const uint32_t world = h->cfg.world, nb = h->cfg.b, base = nb / world, rem = nb % world;
   if (!peer_recv) return fail(h, LSHBLOOM_EUSAGE, "NULL peer_recv");
+  if ((rc = begin_sync(h))) return rc;
   for (uint32_t o = 0; o < world; o++)
     if (!peer_recv[o]) return fail(h, LSHBLOOM_EUSAGE, "NULL receive buffer of rank " + std::to_string(o));
   BandMap m;
@@ -1208,6 +1362,7 @@ int lshbloom_query_insert_bands_peers(lshbloom* h, const uint64_t* bh_owned, uin
   if (world > (uint32_t)kMaxPeers) return fail(h, LSHBLOOM_EUSAGE, "world > 64");
   if (doc_start[0] != 0 || doc_start[world] != n_global)
     return fail(h, LSHBLOOM_EUSAGE, "doc_start must run from 0 to n_global");
+  if ((rc = begin_sync(h))) return rc;
   DupSink sink;
   memset(&sink, 0, sizeof sink);
   sink.npeers = world;
@@ -1229,19 +1384,24 @@ int lshbloom_query_insert_bands_peers(lshbloom* h, const uint64_t* bh_owned, uin
   return LSHBLOOM_OK;
 }
 
+// Stream-ordered: the filters are zeroed on the Bloom stream after every batch enqueued before and
+// before every batch enqueued after, so a reset between async batches does not drain them; with
+// nothing in flight the call also waits for the zeroing (the synchronous behaviour).
 int lshbloom_reset(lshbloom* h) {
   int rc = check_handle(h);
   if (rc) return rc;
   DeviceGuard g(h->device);
+  const bool inflight = h->slot[0].busy || h->slot[1].busy;
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) {
     const size_t tbytes = ((size_t)h->bl << h->c_log2cap) * 8;
-    LB_CUDA(h, cudaMemsetAsync(h->d_ckeys, 0xFF, tbytes, h->own_stream));
-    LB_CUDA(h, cudaMemsetAsync(h->d_cvals, 0xFF, tbytes, h->own_stream));
+    LB_CUDA(h, cudaMemsetAsync(h->d_ckeys, 0xFF, tbytes, h->bloom_stream));
+    LB_CUDA(h, cudaMemsetAsync(h->d_cvals, 0xFF, tbytes, h->bloom_stream));
   } else {
-    LB_CUDA(h, cudaMemsetAsync(h->d_F, 0, (size_t)h->bl * h->W * 4, h->own_stream));
+    LB_CUDA(h, cudaMemsetAsync(h->d_F, 0, (size_t)h->bl * h->W * 4, h->bloom_stream));
   }
-  LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
+  if (!inflight) LB_CUDA(h, cudaStreamSynchronize(h->bloom_stream));
   h->doc_count = 0;
+  for (auto& sl : h->slot) sl.n = 0;      // counted before the reset
   return LSHBLOOM_OK;
 }
 
@@ -1251,7 +1411,8 @@ int lshbloom_filter_copy(lshbloom* h, uint32_t j, uint32_t* dst) {
   if (!dst || j < h->band_lo || j >= h->band_hi) return fail(h, LSHBLOOM_EUSAGE, "band not owned by this handle / NULL dst");
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) return fail(h, LSHBLOOM_EUSAGE, "not a Bloom index");
   DeviceGuard g(h->device);
-  LB_CUDA(h, cudaStreamSynchronize(h->own_stream));
+  if ((rc = drain(h))) return rc;
+  LB_CUDA(h, cudaStreamSynchronize(h->bloom_stream));
   LB_CUDA(h, cudaMemcpy(dst, h->d_F + (uint64_t)(j - h->band_lo) * h->W, h->W * 4, cudaMemcpyDeviceToHost));
   return LSHBLOOM_OK;
 }
@@ -1449,6 +1610,7 @@ int lshbloom_save(lshbloom* h, const char* path) {
   if (h->cfg.index_kind != LSHBLOOM_INDEX_BLOOM) return fail(h, LSHBLOOM_EUSAGE, "save: SPEC's LBF1 format holds standard Bloom filters only");
   if (h->cfg.shingle_n != 5) return fail(h, LSHBLOOM_EUSAGE, "the LSHB format carries no shingle width; save needs n = 5");
   DeviceGuard g(h->device);
+  if ((rc = drain(h))) return rc;
   LB_CUDA(h, cudaDeviceSynchronize());
   FILE* f = fopen(path, "wb");
   if (!f) return fail(h, LSHBLOOM_EIO, std::string("cannot open ") + path + " for writing");
