@@ -63,6 +63,8 @@ def parse():
                     help="N > 1: band-hash / flag exchange over peer memory (default) or NCCL")
     ap.add_argument("--hbm-docs", type=int, default=4_000_000, help="C5 leg: documents per stream batch")
     ap.add_argument("--no-secondary", action="store_true", help="skip the secondary C2 line")
+    ap.add_argument("--sync-steps", action="store_true",
+                    help="one synchronous lshbloom_query_insert per step (default: the async stream form)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle wall time")
     a = ap.parse_args()
     if not a.docs:
@@ -317,6 +319,22 @@ def c5_leg(args, torch, dev, peaks, peak_src):
             stages.append(st)
     fused_ms = statistics.median(times)
     dup_frac = float(out.float().mean().item())
+    # the same batch as a stream: reset + lshbloom_query_insert_async per step, each step's MinHash
+    # overlapping the previous step's Bloom stage; one event pair around all steps
+    for _ in range(2):
+        eng.reset()
+        eng.query_insert_async(d_off, d_tok, out=out)
+    eng.sync()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        eng.reset()
+        eng.query_insert_async(d_off, d_tok, out=out)
+    eng.sync()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    stream_ms = e0.elapsed_time(e1) / steps
     info = eng.info()
     eng.close()
     del eng
@@ -336,6 +354,8 @@ def c5_leg(args, torch, dev, peaks, peak_src):
     torch.cuda.empty_cache()
     return {"workload": "C5 geometry: 128 perms, b=20 r=6, n_expected=1e9 (%.1f GB of filters, m=%d > 2^32), "
                         "%d-document stream batches" % (info["filter_bytes"] / 1e9, info["m"], n),
+            "stream": {"docs_per_s": n / (stream_ms / 1e3), "ms_per_batch": stream_ms, "steps": steps,
+                       "timing": "CUDA events around %d async steps (reset + query_insert_async each)" % steps},
             "fused_step": {"docs_per_s": n / (fused_ms / 1e3), "ms_per_batch": fused_ms,
                            "stages_ms": {"minhash_k1": statistics.median(x[0] for x in stages),
                                          "bloom_stage_span": statistics.median(x[1] for x in stages),
@@ -431,7 +451,12 @@ def main():
                        sub_batch=args.sub_batch, index=args.index)
         sx = None
         d_flags = torch.empty(args.docs, dtype=torch.uint8, device=dev)   # caller-owned output (no allocation per step)
-        step = lambda o, t: eng.query_insert(o, t, out=d_flags)  # noqa: E731
+        # a stream of batches: each step's MinHash overlaps the previous step's Bloom stage
+        # (lshbloom_query_insert_async); --sync-steps times one synchronous call per step instead
+        if args.sync_steps:
+            step = lambda o, t: eng.query_insert(o, t, out=d_flags)  # noqa: E731
+        else:
+            step = lambda o, t: eng.query_insert_async(o, t, out=d_flags)  # noqa: E731
 
     def barrier():
         if world > 1:
@@ -470,6 +495,8 @@ def main():
             if diag:
                 (a, b), _ = eng.stage_times(enable=True)
                 step_stage.append((round(1e3 * (t1 - t0), 2), a, b))
+        if world == 1:
+            eng.sync()                # the batches still in flight (async steps)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         gc.enable()
@@ -493,6 +520,8 @@ def main():
     for _ in range(args.warmup):
         eng.reset()
         flags = step(d_off, d_tok)
+    if world == 1:
+        eng.sync()
     torch.cuda.synchronize(dev)
     eng.stage_times(enable=True)                      # reset accumulators, start recording
     launches0 = eng.launch_count
@@ -515,10 +544,15 @@ def main():
                                                p_tok.to(dev, non_blocking=True)).cpu()
         else:
             h_flags = torch.empty(args.docs, dtype=torch.uint8).pin_memory()
-            e2e_step = lambda: eng.query_insert(p_off, p_tok, out=h_flags)  # noqa: E731
+            if args.sync_steps:
+                e2e_step = lambda: eng.query_insert(p_off, p_tok, out=h_flags)  # noqa: E731
+            else:
+                e2e_step = lambda: eng.query_insert_async(p_off, p_tok, out=h_flags)  # noqa: E731
         for _ in range(max(1, args.warmup // 2)):
             eng.reset()
             e2e_step()
+        if world == 1:
+            eng.sync()
         e2e_ms, _ = timed(e2e_step, args.steps)
         e2e_ms = max_over_ranks(e2e_ms)
         e2e = {"value": n_total * args.steps / (e2e_ms / 1e3), "unit": UNIT,

@@ -20,14 +20,20 @@ struct DevBuf {
   size_t cap = 0;
 };
 
-cudaError_t ensure(DevBuf& b, size_t bytes) {
+// Grow b to at least `bytes` (25 % slack); *fresh (optional) tells whether it was (re)allocated --
+// cudaMalloc may hand back the address it just freed, so callers must not compare pointers.
+cudaError_t ensure(DevBuf& b, size_t bytes, bool* fresh = nullptr) {
+  if (fresh) *fresh = false;
   if (bytes <= b.cap && b.p) return cudaSuccess;
   if (b.p) cudaFree(b.p);
   b.p = nullptr;
   b.cap = 0;
   size_t c = bytes + bytes / 4 + 256;
   cudaError_t e = cudaMalloc(&b.p, c);
-  if (e == cudaSuccess) b.cap = c;
+  if (e == cudaSuccess) {
+    b.cap = c;
+    if (fresh) *fresh = true;
+  }
   return e;
 }
 
@@ -579,9 +585,11 @@ SweepPlan plan_sweep(const lshbloom* h, uint64_t n) {
     if (!two) return sweep_cap_for(mu);
     return (sweep_cap_for(mu, 3.0) + 15u) & ~15u;
   };
+  // windows up to 2^17 bits (16 KB: four K8 CTAs per SM fit; C5 4M-document sweeps measured
+  // 36.4 ms at 2^17 vs 38.0 ms at 2^18 with two CTAs per SM)
   const bool two = h->k == 17;
   uint32_t wb = 10;
-  while (wb < 19 && fine_cap(wb + 1, two) <= kSweepCapReg) wb++;
+  while (wb < 17 && fine_cap(wb + 1, two) <= kSweepCapReg) wb++;
   if (h->sweep_wb_force) wb = h->sweep_wb_force;
   if (h->bloom_path == LSHBLOOM_PATH_AUTO) {
     const double fbytes = (double)h->bl * (double)h->W * 4.0;
@@ -603,9 +611,9 @@ SweepPlan plan_sweep(const lshbloom* h, uint64_t n) {
 
 // ensure() for buffers that must start zeroed (the miss words are re-zeroed by K9 after use).
 int ensure_zeroed(lshbloom* h, DevBuf& b, size_t bytes, cudaStream_t s) {
-  void* before = b.p;
-  LB_CUDA(h, ensure(b, bytes));
-  if (b.p != before) LB_CUDA(h, cudaMemsetAsync(b.p, 0, b.cap, s));
+  bool fresh = false;
+  LB_CUDA(h, ensure(b, bytes, &fresh));
+  if (fresh) LB_CUDA(h, cudaMemsetAsync(b.p, 0, b.cap, s));
   return LSHBLOOM_OK;
 }
 
@@ -668,6 +676,20 @@ int sweep_finish(lshbloom* h, const SweepParams& p, cudaStream_t s, bool first, 
   if (first) stage_begin(h, 2, s);
   h->launches += launch_sweep_finish(p, sweep_grid(h->sm_count, p.wb), s);
   LB_CUDA(h, cudaGetLastError());
+  if (getenv("LSHBLOOM_SWEEP_DEBUG")) {   // diagnostic: record counts of the bins
+    cudaStreamSynchronize(s);
+    std::vector<uint32_t> cur(p.nbins), cc(p.two_level ? p.g.bl * p.ncb : 0);
+    uint32_t ovf = 0;
+    cudaMemcpy(cur.data(), p.cursor, p.nbins * 4, cudaMemcpyDeviceToHost);
+    if (p.two_level) cudaMemcpy(cc.data(), p.ccursor, cc.size() * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&ovf, p.ovf, 4, cudaMemcpyDeviceToHost);
+    uint64_t sf = 0, sc = 0, mf = 0, mc = 0;
+    for (auto v : cur) { sf += v; mf = std::max<uint64_t>(mf, v); }
+    for (auto v : cc) { sc += v; mc = std::max<uint64_t>(mc, v); }
+    fprintf(stderr, "sweep n=%u wb=%u cap=%u two=%u cb=%u ncb=%lu ccap=%u ovf=%u records=%lu fine_sum=%lu fine_max=%lu coarse_sum=%lu coarse_max=%lu\n",
+            p.n, p.wb, p.cap, p.two_level, p.cb, (unsigned long)p.ncb, p.ccap, ovf, (unsigned long)((uint64_t)p.n * h->k * h->bl),
+            (unsigned long)sf, (unsigned long)mf, (unsigned long)sc, (unsigned long)mc);
+  }
   if (last) stage_end(h, 2, s);
   h->sweeps++;
   return LSHBLOOM_OK;
@@ -781,8 +803,17 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
   // the next chunk's K1) and every piece of <= kSweepMaxDocs documents is swept once complete;
   // chunk boundaries fall on piece boundaries.
   const SweepPlan sp = plan_sweep(h, n);
+  // With the sweep the Bloom work per chunk is only the binning, so K1 runs in larger chunks (a
+  // K1 launch ends with a tail on a few warps; fewer launches, fewer tails):
+  // LSHBLOOM_FUSE_DOCS_SWEEP documents per chunk.
+  static const uint64_t sweep_chunk = [] {
+    const char* e = getenv("LSHBLOOM_FUSE_DOCS_SWEEP");
+    return e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : (uint64_t)262144;
+  }();
   auto clip = [&](uint64_t d0, uint64_t d1) {
-    return sp.use ? std::min(d1, (d0 / kSweepMaxDocs + 1) * kSweepMaxDocs) : d1;
+    if (!sp.use) return d1;
+    d1 = std::max(d1, std::min(n, d0 + sweep_chunk));
+    return std::min(d1, (d0 / kSweepMaxDocs + 1) * kSweepMaxDocs);
   };
   // Chunk bounds first, all of them checked before anything is enqueued: a host batch's copies
   // read tokens [offsets[d0], offsets[d1]) of the caller's buffer, so every bound must satisfy

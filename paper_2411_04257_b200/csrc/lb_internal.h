@@ -126,6 +126,7 @@ struct SweepParams {
   uint64_t* miss;            // [n] bit jl set: band jl of sweep document d missed
   uint32_t* eg;              // [grid][2^wb] earliest setter per position, for bins beyond kSweepCapReg
   uint32_t i0, n;            // this sweep = batch documents [i0, i0 + n)
+  uint32_t stages;           // K8 pipeline depth (windows + records in flight per CTA)
   // two-level binning (k = 17): K7a sorts each 512-document tile's records by coarse bucket
   // (2^cb windows) in shared memory and writes them as runs; K7b re-sorts each coarse bucket by
   // window in 4096-record chunks -- every record is written in coalesced runs, never scattered
@@ -163,7 +164,9 @@ int launch_bloom_subbatch(const BloomParams& p, int sm_count, cudaStream_t s);
 int launch_classic(const ClassicParams& p, cudaStream_t s);
 int launch_sweep_bin(const SweepParams& p, uint32_t lo, uint32_t hi, cudaStream_t s);
 int launch_sweep_finish(const SweepParams& p, int grid, cudaStream_t s);
-int sweep_grid(int sm_count, uint32_t wb);     // K8 CTAs (persistent) for a window size
+struct SweepLaunch { int grid; uint32_t stages; size_t smem; };
+SweepLaunch sweep_launch_cfg(int sm_count, uint32_t wb);   // K8 persistent grid / pipeline depth
+int sweep_grid(int sm_count, uint32_t wb);                 // = sweep_launch_cfg().grid
 int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t bl, cudaStream_t s);
 constexpr int kSweepThreads = 256;               // K8 block size
 constexpr int kSweepRPT = 4;                     // records per thread held in registers

@@ -63,6 +63,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -302,13 +307,15 @@ __global__ void __launch_bounds__(kSweepTileDocs, 1) k7a_coarse(const SweepParam
 // K7b: one coarse bucket per CTA (grid: bl * ncb).  The CTA owns the bucket's windows, so their
 // write positions are shared-memory counters (no global atomics); records are staged per window
 // in shared memory and written 16 at a time -- whole 128-byte lines -- as they accumulate.
-constexpr size_t k7b_smem_bytes() { return (size_t)kSweepMaxW * (kSweepStage * 8 + 8); }
+constexpr size_t k7b_smem_bytes() { return (size_t)kSweepMaxW * (kSweepStage * 8 + 12) + 16; }
 
 __global__ void __launch_bounds__(kSweepBThreads) k7b_fine(const SweepParams p) {
   extern __shared__ __align__(16) uint8_t dsm[];
   uint64_t(*stage)[kSweepStage] = (uint64_t(*)[kSweepStage])dsm;
   uint32_t* scnt = (uint32_t*)(dsm + (size_t)kSweepMaxW * kSweepStage * 8);
   uint32_t* gcur = scnt + kSweepMaxW;
+  uint32_t* fullq = gcur + kSweepMaxW;                   // windows that reached 16 staged records
+  uint32_t* nfull = fullq + kSweepMaxW;
   constexpr uint32_t RPT = kSweepChunk / kSweepBThreads;
   if (*p.g.err || *p.ovf) return;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -321,6 +328,7 @@ __global__ void __launch_bounds__(kSweepBThreads) k7b_fine(const SweepParams p) 
   const uint64_t bin0 = (uint64_t)jl * p.nw + (uint64_t)cbk * W;
   const uint64_t wmask = (1ull << p.wb) - 1;
   for (uint32_t w = tid; w < W; w += blockDim.x) scnt[w] = gcur[w] = 0;
+  if (tid == 0) *nfull = 0;
   __syncthreads();
   bool over = false;
   auto out = [&](uint32_t w) { return p.rec + (bin0 + w) * p.cap; };
@@ -339,6 +347,7 @@ __global__ void __launch_bounds__(kSweepBThreads) k7b_fine(const SweepParams p) 
       const uint32_t slot = atomicAdd(&scnt[w], 1u);
       if (slot < kSweepStage) {
         stage[w][slot] = rec;
+        if (slot == 15) fullq[atomicAdd(nfull, 1u)] = w;   // a whole line is ready
       } else {                                             // staging full (rare): write it now
         const uint32_t o = atomicAdd(&gcur[w], 1u);
         if (o < p.cap) out(w)[o] = rec;
@@ -346,7 +355,11 @@ __global__ void __launch_bounds__(kSweepBThreads) k7b_fine(const SweepParams p) 
       }
     }
     __syncthreads();
-    for (uint32_t w = warp; w < nwin; w += nwarps) {     // flush whole lines
+    const uint32_t nf = *nfull;
+    __syncthreads();                                     // everyone has read the count
+    if (tid == 0) *nfull = 0;                            // (appends resume after the next barrier)
+    for (uint32_t fi = warp; fi < nf; fi += nwarps) {    // flush whole lines of the full windows
+      const uint32_t w = fullq[fi];
       const uint32_t c = min(scnt[w], kSweepStage), full = c & ~15u;
       if (full) {
         const uint32_t base = gcur[w];
@@ -362,8 +375,6 @@ __global__ void __launch_bounds__(kSweepBThreads) k7b_fine(const SweepParams p) 
           gcur[w] = base + full;
           scnt[w] = c - full;
         }
-      } else if (lane == 0) {
-        scnt[w] = c;
       }
       __syncwarp();
     }
@@ -427,19 +438,21 @@ int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t 
 __device__ __forceinline__ uint32_t ehash(uint32_t gl) { return (gl * 0x9E3779B1u) >> (32 - kEcapLog2); }
 __device__ __forceinline__ uint32_t shash(uint32_t gl) { return (gl * 0x85EBCA77u) >> (32 - kSummLog2); }
 
-// earliest setter table in shared memory: slot = gl << 32 | doc, min doc per gl
-__device__ __forceinline__ void e_insert_min(uint64_t* etab, uint32_t gl, uint32_t doc) {
+// earliest setter table in shared memory: slot = gl << 32 | doc, min doc per gl.  Returns the
+// slot, which the inserting record empties again after the window (the table is never cleared
+// wholesale: a window has only a handful of contested positions).
+__device__ __forceinline__ uint32_t e_insert_min(uint64_t* etab, uint32_t gl, uint32_t doc) {
   const uint64_t packed = ((uint64_t)gl << 32) | doc;
   uint32_t s = ehash(gl);
   for (;;) {
     uint64_t cur = *(volatile uint64_t*)(etab + s);
     if (cur == kEEmpty) {
       cur = atomicCAS((unsigned long long*)(etab + s), (unsigned long long)kEEmpty, (unsigned long long)packed);
-      if (cur == kEEmpty) return;
+      if (cur == kEEmpty) return s;
     }
     if ((uint32_t)(cur >> 32) == gl) {
       atomicMin((unsigned long long*)(etab + s), (unsigned long long)packed);
-      return;
+      return s;
     }
     s = (s + 1) & (kEcap - 1);
   }
@@ -460,63 +473,93 @@ __device__ __forceinline__ uint32_t e_find_min(const uint64_t* etab, uint32_t gl
 __host__ __device__ constexpr uint32_t k8_rec_bytes() { return kSweepCapReg * 8; }
 __host__ __device__ inline uint32_t k8_stage_bytes(uint32_t wb) { return ((1u << wb) >> 3) + k8_rec_bytes(); }
 
-// Persistent CTAs stride over the window bins; while one bin is processed the next non-empty
-// bin's window and records are already in flight (TMA bulk copies into the other stage).
+// Persistent CTAs stride over the window bins.  A ring of p.stages stages keeps the windows and
+// records of the next stages-1 non-empty bins in flight (TMA bulk copies) while one is processed.
+struct K8Meta {                      // per stage, written by thread 0 when it issues the copies
+  uint64_t bin;                      // ~0: no more bins
+  uint32_t* gwin;
+  uint32_t jl, R, bytes, pad;
+};
+
 __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr uint32_t kMaxStages = 8;
+  __shared__ K8Meta meta[kMaxStages];
+  const uint32_t S = p.stages;
   const uint32_t wbytes_max = (1u << p.wb) >> 3, stage = k8_stage_bytes(p.wb);
-  uint64_t* etab = (uint64_t*)(smem + 2 * stage);
+  uint64_t* etab = (uint64_t*)(smem + S * stage);
   uint32_t* summ = (uint32_t*)(etab + kEcap);
   uint64_t* bar = (uint64_t*)(summ + (1u << kSummLog2) / 32);
   if (*p.g.err) return;
   const uint32_t tid = threadIdx.x, T = blockDim.x;
   const bool exact = *p.ovf != 0;
-  if (tid == 0) {
-    mbar_init(bar);
-    mbar_init(bar + 1);
-  }
-  __syncthreads();
-  uint32_t parity[2] = {0, 0};
-  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
+  const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last(),
+                 pol_normal = policy_evict_normal();
   const uint64_t wwords = (uint64_t)1 << (p.wb - 5);
-  const uint64_t G = gridDim.x;
   uint32_t* eg = p.eg + (uint64_t)blockIdx.x * (1ull << p.wb);
-  auto next_bin = [&](uint64_t b) {
-    while (b < p.nbins && p.cursor[b] == 0) b += G;         // untouched windows are skipped
-    return b;
-  };
-  auto geom = [&](uint64_t bin, uint32_t& jl, uint32_t*& gwin, uint32_t& bytes) {
-    jl = (uint32_t)(bin / p.nw);
-    const uint64_t w = bin - (uint64_t)jl * p.nw;
-    gwin = p.g.F + (uint64_t)jl * p.g.W + w * wwords;
-    bytes = (uint32_t)(umin64(wwords, p.g.W - w * wwords) * 4);
-  };
   // records go through shared memory with the window when they can (fixed layout, register path)
   auto staged = [&](uint32_t R) { return !exact && R <= kSweepCapReg; };
-  auto issue = [&](uint64_t bin, int st) {                  // thread 0
-    uint32_t jl, bytes;
-    uint32_t* gwin;
-    geom(bin, jl, gwin, bytes);
-    const uint32_t R = p.cursor[bin];
-    const uint32_t rb = staged(R) ? ((R * 8 + 15) & ~15u) : 0;
-    uint8_t* sb = smem + st * stage;
-    mbar_expect_tx(bar + st, bytes + rb);
-    bulk_load(sb, gwin, bytes, bar + st, pol_stream);
-    if (rb) bulk_load(sb + wbytes_max, p.rec + bin * p.cap, rb, bar + st, pol_stream);
-  };
-  uint64_t bin = next_bin(blockIdx.x);
-  if (tid == 0 && bin < p.nbins) issue(bin, 0);
-  int st = 0;
-  while (bin < p.nbins) {
-    const uint64_t nb = next_bin(bin + G);
-    if (tid == 0 && nb < p.nbins) {
-      bulk_wait_read_all();                                  // the other stage's window store has left smem
-      issue(nb, st ^ 1);
+  // Thread 0 walks this CTA's bins (bin = blockIdx.x + k * gridDim.x, band-major: band jl, window
+  // w), skipping untouched windows, and issues each one's copies into the next free stage.
+  uint64_t nb = blockIdx.x, nw_w = 0;
+  uint32_t nb_jl = 0;
+  if (tid == 0) {
+    nb_jl = (uint32_t)(nb / p.nw);
+    nw_w = nb - (uint64_t)nb_jl * p.nw;
+  }
+  auto advance = [&]() {                                     // thread 0: to the next non-empty bin
+    while (nb < p.nbins && p.cursor[nb] == 0) {
+      nb += gridDim.x;
+      nw_w += gridDim.x;
+      while (nw_w >= p.nw) { nw_w -= p.nw; nb_jl++; }
     }
-    uint32_t jl, bytes;
-    uint32_t* gwin;
-    geom(bin, jl, gwin, bytes);
-    const uint32_t R = p.cursor[bin];
+  };
+  auto issue = [&](uint32_t st) {                            // thread 0: bin nb -> stage st
+    K8Meta m;
+    m.bin = ~0ull;
+    if (nb < p.nbins) {
+      m.bin = nb;
+      m.jl = nb_jl;
+      m.gwin = p.g.F + (uint64_t)nb_jl * p.g.W + nw_w * wwords;
+      m.bytes = (uint32_t)(umin64(wwords, p.g.W - nw_w * wwords) * 4);
+      m.R = p.cursor[nb];
+      const uint32_t rb = staged(m.R) ? ((m.R * 8 + 15) & ~15u) : 0;
+      uint8_t* sb = smem + st * stage;
+      mbar_expect_tx(bar + st, m.bytes + rb);
+      bulk_load(sb, m.gwin, m.bytes, bar + st, pol_stream);
+      if (rb) bulk_load(sb + wbytes_max, p.rec + nb * p.cap, rb, bar + st, pol_stream);
+      nb += gridDim.x;
+      nw_w += gridDim.x;
+      while (nw_w >= p.nw) { nw_w -= p.nw; nb_jl++; }
+    }
+    meta[st] = m;
+  };
+  if (tid == 0) {
+    for (uint32_t i = 0; i < S; i++) mbar_init(bar + i);
+    for (uint32_t i = 0; i + 1 < S; i++) {                   // prologue: S - 1 stages in flight
+      advance();
+      issue(i);
+    }
+  }
+  for (uint32_t q = tid; q < kEcap; q += T) etab[q] = kEEmpty;          // kept empty between windows
+  for (uint32_t q = tid; q < (1u << kSummLog2) / 32; q += T) summ[q] = 0;
+  __syncthreads();
+  uint32_t parity_bits = 0;                                  // bit i: phase of stage i's barrier
+  uint32_t st = 0;
+  for (;;) {
+    const K8Meta m = meta[st];
+    if (m.bin == ~0ull) break;
+    const uint32_t fill = st == 0 ? S - 1 : st - 1;          // the stage processed last iteration
+    if (tid == 0) {
+      bulk_wait_read_all();                                  // its window store has left smem
+      advance();
+      issue(fill);                                           // (published to all by the barriers below)
+    }
+    const uint32_t parity = (parity_bits >> st) & 1u;
+    parity_bits ^= 1u << st;
+    const uint64_t bin = m.bin;
+    const uint32_t jl = m.jl, bytes = m.bytes, R = m.R;
+    uint32_t* gwin = m.gwin;
     uint32_t* win = (uint32_t*)(smem + st * stage);
     const uint64_t* srec = (const uint64_t*)(smem + st * stage + wbytes_max);
     const uint64_t* rec = p.rec + (exact ? p.start[bin] : bin * p.cap);
@@ -524,8 +567,6 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
     const uint64_t bitj = 1ull << jl;
     if (R <= kSweepCapReg) {
       // ---- records in registers, earliest setters in a shared table
-      for (uint32_t q = tid; q < kEcap; q += T) etab[q] = kEEmpty;
-      for (uint32_t q = tid; q < (1u << kSummLog2) / 32; q += T) summ[q] = 0;
       uint64_t r[kSweepRPT];
       if (!staged(R)) {
 #pragma unroll
@@ -534,8 +575,7 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
           r[q] = idx < R ? ld_stream(rec + idx, pol_stream) : ~0ull;
         }
       }
-      mbar_wait(bar + st, parity[st]);
-      parity[st] ^= 1;
+      mbar_wait(bar + st, parity);
       if (staged(R)) {
 #pragma unroll
         for (int q = 0; q < kSweepRPT; q++) {
@@ -544,6 +584,8 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
         }
       }
       uint32_t pre = 0, first = 0;                           // per-record flags (bit q)
+      bool touched = false;                                  // this thread wrote etab / summ
+      uint32_t es[kSweepRPT];                                // etab slot each record entered
 #pragma unroll
       for (int q = 0; q < kSweepRPT; q++) {
         if (r[q] == ~0ull) { pre |= 1u << q; continue; }     // (padding: treated as pre-set)
@@ -561,14 +603,14 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
         if (old & bit) {                                     // contested: another record set it
           const uint32_t h = shash(gl);
           atomicOr(summ + (h >> 5), 1u << (h & 31));
-          e_insert_min(etab, gl, doc);
+          es[q] = e_insert_min(etab, gl, doc);
+          touched = true;
         } else {
           first |= 1u << q;
         }
       }
+      fence_proxy_async();                                   // this thread's window writes -> async proxy
       __syncthreads();                                       // window final, summary complete
-      fence_proxy_async();
-      __syncthreads();
       if (tid == 0) bulk_store(gwin, win, bytes, pol_stream);
       uint32_t joined = 0;
 #pragma unroll
@@ -577,8 +619,9 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
         const uint32_t gl = (uint32_t)(r[q] >> 32);
         const uint32_t h = shash(gl);
         if ((summ[h >> 5] >> (h & 31)) & 1u) {               // (possibly) contested position
-          e_insert_min(etab, gl, (uint32_t)r[q]);
+          es[q] = e_insert_min(etab, gl, (uint32_t)r[q]);
           joined |= 1u << q;
+          touched = true;
         }
       }
       __syncthreads();
@@ -590,14 +633,24 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
         if (!((first >> q) & 1) || ((joined >> q) & 1)) set_before = e_find_min(etab, gl) < doc;
         if (!set_before) red_or_keep(p.miss + doc, bitj, pol_keep);
       }
-      __syncthreads();                                       // table reads done before the next clear
+      __syncthreads();                                       // every table read done
+      if (touched) {                                         // empty what this thread filled
+#pragma unroll
+        for (int q = 0; q < kSweepRPT; q++) {
+          if ((pre >> q) & 1) continue;
+          if (((first >> q) & 1) && !((joined >> q) & 1)) continue;
+          const uint32_t h = shash((uint32_t)(r[q] >> 32));
+          summ[h >> 5] = 0;
+          etab[es[q]] = kEEmpty;
+        }
+      }
+      // (the next window's inserts come after its first barrier, so no barrier is needed here)
     } else {
       // ---- a bin beyond kSweepCapReg records: records streamed from global memory, earliest
       // setters in this CTA's direct-mapped global array (one entry per window position)
       const uint32_t np = 1u << p.wb;
       for (uint32_t q = tid; q < np; q += T) eg[q] = 0xFFFFFFFFu;
-      mbar_wait(bar + st, parity[st]);
-      parity[st] ^= 1;
+      mbar_wait(bar + st, parity);
       uint64_t* wrec = p.rec + (exact ? p.start[bin] : bin * p.cap);
       for (uint32_t idx = tid; idx < R; idx += T) {
         const uint64_t rr = wrec[idx];
@@ -625,8 +678,8 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
       }
       __syncthreads();
     }
-    bin = nb;
-    st ^= 1;
+    st = st + 1 == S ? 0 : st + 1;
+    __syncthreads();                                         // meta[fill] published before it is read
   }
   if (tid == 0) bulk_wait_all();
 }
@@ -705,24 +758,46 @@ static void count_dispatch(const SweepParams& p, cudaStream_t s) {
   else kf_count<0, uint64_t, ProbeGen><<<grid, SW_BIN_THREADS, 0, s>>>(p, p.i0, p.n);
 }
 
-static size_t sweep_smem(uint32_t wb) {
-  return 2 * (size_t)k8_stage_bytes(wb) + kEcap * 8 + (1u << kSummLog2) / 8 + 16;
+static size_t sweep_smem(uint32_t wb, uint32_t stages) {
+  return (size_t)stages * k8_stage_bytes(wb) + kEcap * 8 + (1u << kSummLog2) / 8 + 8 * 8;
 }
 
-int sweep_grid(int sm_count, uint32_t wb) {
-  const size_t sm = sweep_smem(wb);
+// K8: persistent CTAs, as many per SM as fit (LSHBLOOM_K8_CTAS caps it), each with a ring of
+// `stages` pipeline stages (LSHBLOOM_K8_STAGES, default 2).  The grid never exceeds what is
+// resident at once (a second wave of persistent CTAs would serialise).
+SweepLaunch sweep_launch_cfg(int sm_count, uint32_t wb) {
+  static const int env_ctas = [] { const char* e = getenv("LSHBLOOM_K8_CTAS"); return e ? atoi(e) : 0; }();
+  static const int env_st = [] { const char* e = getenv("LSHBLOOM_K8_STAGES"); return e ? atoi(e) : 0; }();
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k8_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem(19));
+    // (227 KB per block minus K8's static meta array)
+    cudaFuncSetAttribute(k8_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024);
     attr = true;
   }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k8_sweep, kSweepThreads, sm) != cudaSuccess || per_sm < 1)
+  uint32_t st = env_st ? (uint32_t)env_st : 2u;
+  st = st < 2 ? 2 : st > 8 ? 8 : st;
+  while (st > 2 && sweep_smem(wb, st) > 224 * 1024) st--;
+  SweepLaunch c;
+  c.stages = st;
+  c.smem = sweep_smem(wb, st);
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k8_sweep, kSweepThreads, c.smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
-  return sm_count * per_sm;
+  // K8 is bound by its per-window barrier phases, not by HBM latency: more resident CTAs help
+  // (C5 geometry, 16 KB windows: 4 per SM 29.9 ms vs 2 per SM 36.1 ms for K7b + K8), deeper
+  // pipelines do not (2 / 3 / 4 stages within 0.1 ms)
+  if (env_ctas > 0 && env_ctas < per_sm) per_sm = env_ctas;
+  c.grid = sm_count * per_sm;
+  return c;
 }
 
-int launch_sweep_finish(const SweepParams& p, int grid, cudaStream_t s) {
+int sweep_grid(int sm_count, uint32_t wb) { return sweep_launch_cfg(sm_count, wb).grid; }
+
+int launch_sweep_finish(const SweepParams& p_in, int grid_unused, cudaStream_t s) {
+  (void)grid_unused;
+  SweepParams p = p_in;
+  const SweepLaunch lc = sweep_launch_cfg(0, p.wb);
+  p.stages = lc.stages;
   int l = 0;
   if (p.two_level) {
     static bool attr = false;
@@ -738,7 +813,10 @@ int launch_sweep_finish(const SweepParams& p, int grid, cudaStream_t s) {
   count_dispatch(p, s);
   k7_scan<<<1, 1024, 0, s>>>(p);
   bin_dispatch(p, p.i0, p.i0 + p.n, true, s);
-  k8_sweep<<<grid, kSweepThreads, sweep_smem(p.wb), s>>>(p);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k8_sweep<<<sweep_launch_cfg(sms, p.wb).grid, kSweepThreads, lc.smem, s>>>(p);
   k9_verdict<<<(p.n + 255) / 256, 256, 0, s>>>(p);
   return l + 6;
 }
