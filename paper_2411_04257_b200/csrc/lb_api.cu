@@ -810,9 +810,10 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
     const char* e = getenv("LSHBLOOM_FUSE_DOCS_SWEEP");
     return e ? std::max<uint64_t>(1024, strtoull(e, nullptr, 10)) : (uint64_t)262144;
   }();
+  // (host batches keep their staging-sized chunks: those overlap the H2D copy with K1)
   auto clip = [&](uint64_t d0, uint64_t d1) {
     if (!sp.use) return d1;
-    d1 = std::max(d1, std::min(n, d0 + sweep_chunk));
+    if (b->on_device) d1 = std::max(d1, std::min(n, d0 + sweep_chunk));
     return std::min(d1, (d0 / kSweepMaxDocs + 1) * kSweepMaxDocs);
   };
   // Chunk bounds first, all of them checked before anything is enqueued: a host batch's copies

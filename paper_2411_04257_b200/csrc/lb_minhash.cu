@@ -518,6 +518,173 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Screened K1, lean form (warp per document).  Same screen and the same exactness argument as
+// k1_minhash_scr, with less state per lane so that more warps are resident (the screened loop
+// stalls on fixed-latency dependencies -- "wait" -- with the 4 warps per scheduler the 127-register
+// kernel allows):
+//  * per permutation only a0, a1 (the screen's multipliers), bias = b0 - m and K = 2^32 - 5 - m
+//    live in registers; m = 2^32 - 5 - K is implicit, b0 / b1 are re-read (L1) on an update;
+//  * each screen that admits a candidate sets a bit in a per-permutation mask over the chunk's
+//    32 shingles (ISETP + a predicated LOP3) instead of queueing it in shared memory (STS + add);
+//    the candidates are evaluated exactly at the end of the chunk, all lanes in step;
+//  * PASSES > 1 walks the document PASSES times with NPL permutations each (the fingerprints are
+//    recomputed, ~2 % of the work) -- 256 permutations as 2 x 4 per lane.
+template <int NPL, int PASSES, int MINB = 3>
+__global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr2(const MinhashParams p) {
+  __shared__ XLimbs xs[K1_WARPS][32];
+  __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (*p.err) return;
+  if (p.block_gate && p.list && *p.list_n < p.block_gate) return;   // the block-per-document kernel runs
+  const uint64_t tpol = l2_evict_first_policy();
+  const uint32_t sh29 = p.sh29;
+
+  for (;;) {
+    uint32_t di = 0;
+    if (lane == 0) di = atomicAdd(p.counter, 1u);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (di >= (p.list ? *p.list_n : p.n_docs)) break;
+    const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
+    const uint64_t o0 = p.offsets[d];
+    const uint64_t L = p.offsets[d + 1] - o0;
+    LB_ASSERT(L >= 1 && o0 >= p.tok_base);
+    const uint32_t* tk = p.tokens + (o0 - p.tok_base);
+    const uint32_t n = p.shingle_n;
+    const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;
+    const uint32_t t = L >= n ? n : (uint32_t)L;
+    const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
+
+    for (int pass = 0; pass < PASSES; pass++) {
+      const uint32_t pm0 = pass * 32 * NPL + lane;           // permutation of slot q: pm0 + 32 q
+      uint32_t a0[NPL], a1[NPL], bias[NPL], K[NPL];
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const PermCoef c = p.coef[pm0 + 32 * q];
+        a0[q] = c.a0;
+        a1[q] = c.a1;
+      }
+      bool exact_mode = false;
+      for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        if (s < S) {
+          uint64_t h = init;
+          for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
+          xs[w][lane] = make_limbs(h);
+        }
+        __syncwarp();
+        const uint32_t cnt = min(32u, S - s0);
+        uint32_t j = 0;
+        if (s0 == 0) {   // seed the minima with the first shingle, exactly
+          const XLimbs x0 = xs[w][0];
+          bool big = false;
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);     // (the raw minimum, for now)
+            big |= K[q] > 0xFFFFFFFBu;
+          }
+          exact_mode = __any_sync(0xffffffffu, big);
+          if (!exact_mode) {
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+              bias[q] = p.coef[pm0 + 32 * q].b0 - K[q];
+              K[q] = 0xFFFFFFFBu - K[q];
+            }
+          }
+          j = 1;
+        }
+        if (exact_mode) {     // (probability ~2^-30 per document) K holds the raw minima
+          for (; j < cnt; j++) {
+            const XLimbs xv = xs[w][j];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(p.coef[pm0 + 32 * q], xv));
+          }
+        } else {
+          uint32_t rsh29;
+          asm volatile("mov.u32 %0, %1;" : "=r"(rsh29) : "r"(sh29));   // opaque: shift stays on the ALU pipe
+          uint32_t mask[NPL];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) mask[q] = 0;
+          for (; j + 4 <= cnt; j += 4) {
+            XLimbs xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) xv[u] = xs[w][j + u];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+              const PermCoef cq = {a0[q], a1[q], 0u, 0u};
+#pragma unroll
+              for (int u = 0; u < 4; u++)
+                if (screen(cq, xv[u], bias[q], K[q], rsh29)) mask[q] |= 1u << (j + u);
+            }
+          }
+          for (; j < cnt; j++) {
+            const XLimbs xv = xs[w][j];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+              const PermCoef cq = {a0[q], a1[q], 0u, 0u};
+              if (screen(cq, xv, bias[q], K[q], rsh29)) mask[q] |= 1u << j;
+            }
+          }
+          // exact evaluation of the candidates, all lanes in step (rounds = the warp's largest count)
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            const uint32_t rounds = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(mask[q]));
+            if (!rounds) continue;
+            const PermCoef c = p.coef[pm0 + 32 * q];
+            for (uint32_t i = 0; i < rounds; i++) {
+              if (mask[q]) {
+                const uint32_t js = __ffs(mask[q]) - 1;
+                mask[q] &= mask[q] - 1;
+                const uint32_t y = eval_exact(c, xs[w][js]);
+                if (y < 0xFFFFFFFBu - K[q]) {
+                  bias[q] = c.b0 - y;
+                  K[q] = 0xFFFFFFFBu - y;
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const uint32_t m = exact_mode ? K[q] : 0xFFFFFFFBu - K[q];
+        const uint32_t pm = pm0 + 32 * q;
+        if (p.sig_out && pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = m;
+        if (p.bh_out) sg[w][pm] = m;
+      }
+    }  // pass
+    if (p.bh_out) {
+      __syncwarp();
+      for (uint32_t jb = lane; jb < p.b; jb += 32) {
+        if (p.map.ncol[jb] == 0) continue;
+        uint64_t acc = 0;                               // BH_j, P:207-208 (DESIGN R6/R7)
+        for (uint32_t u = 0; u < p.r; u++) {
+          acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][jb * p.r + u], __ldg(p.bcoef + p.r + u));
+          acc = acc >= kP ? acc - kP : acc;
+        }
+        p.map.ptr[jb][(uint64_t)d * p.map.ncol[jb]] = acc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int NPL, int PASSES, int MINB = 3>
+static int launch_s2(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash_scr2<NPL, PASSES, MINB>, K1_THREADS, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
+  const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
+  uint64_t grid = (uint64_t)sm_count * bps;
+  if (want < grid) grid = want ? want : 1;
+  k1_minhash_scr2<NPL, PASSES, MINB><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  return 1;
+}
+
 template <int NPL, bool BLOCKDOC = false>
 static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int blocks_per_sm = 0;
@@ -596,7 +763,12 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     // the one the device-side count does not select returns at once
     b.block_gate = 16u * (uint32_t)sm_count * 2u * K1_WARPS;
     cudaMemsetAsync(p.counter, 0, 4, s);
-    launch_s<8, false>(b, sm_count, s, max_bps);
+    // warp-per-document long documents: the lean screened kernel (80 registers, 3 blocks per SM;
+    // C3 200K full texts alone: 102.0 ms vs 111.4 ms for k1_minhash_scr; 2 x 4 permutations per
+    // lane at 4 blocks: 108.2 ms; LSHBLOOM_K1_SCR=1 selects the older kernel)
+    static const int scr = [] { const char* e = getenv("LSHBLOOM_K1_SCR"); return e ? atoi(e) : 2; }();
+    if (scr == 1) launch_s<8, false>(b, sm_count, s, max_bps);
+    else launch_s2<8, 1>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
     return 4;
