@@ -226,6 +226,25 @@ LSHBLOOM_API int lshbloom_sync(lshbloom *h);
 LSHBLOOM_API int lshbloom_query_insert_bands(lshbloom *h, const uint64_t *bh_owned, uint64_t n_docs,
                                 int32_t on_device, void *stream, uint8_t *hit_out);
 
+/* A batch of the owned bands assembled from band-hash chunks, for pipelined sharded steps: the
+ * chunks of the global batch can be handed over in any order (disjoint document ranges, global
+ * stream order is the document index), and with the window sweep each chunk's probes are binned
+ * as soon as it arrives -- so the exchange and binning of chunk c overlap the MinHash of chunk
+ * c+1 on every rank -- while the query-then-insert itself runs at finish in exact stream order.
+ *  lshbloom_bands_begin(h, n_global): start a batch of n_global (< 2^32) documents (waits for
+ *    earlier work of the handle).
+ *  lshbloom_bands_add(h, bh_owned, doc0, n_docs, stream): bh_owned = device [n_docs][band_hi -
+ *    band_lo] band hashes of global documents [doc0, doc0 + n_docs), produced on `stream`;
+ *    copied into the batch (stream-ordered: reusable once `stream` passes this call).
+ *  lshbloom_bands_finish(h, hit_out, stream): every document added exactly once, else error 1;
+ *    hit_out (device, n_global) = OR over the owned bands of the stream-order verdicts, as
+ *    lshbloom_query_insert_bands would give for the whole batch.  Mutates the filters;
+ *    synchronises. */
+LSHBLOOM_API int lshbloom_bands_begin(lshbloom *h, uint64_t n_global);
+LSHBLOOM_API int lshbloom_bands_add(lshbloom *h, const uint64_t *bh_owned, uint64_t doc0, uint64_t n_docs,
+                                    void *stream);
+LSHBLOOM_API int lshbloom_bands_finish(lshbloom *h, uint8_t *hit_out, void *stream);
+
 /* Band-sharded exchange over peer memory (world > 1 on GPUs with
  * peer access, e.g. NVLink / NVSwitch via torch symmetric memory).  Instead of an owner-major
  * local buffer + all-to-all + all-reduce:

@@ -65,7 +65,7 @@ EXPORTS = ("lshbloom_create", "lshbloom_create_ex", "lshbloom_destroy", "lshbloo
            "lshbloom_stage_times", "lshbloom_save", "lshbloom_load", "lshbloom_last_error",
            "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan",
            "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers", "lshbloom_query_insert_async",
-           "lshbloom_sync")
+           "lshbloom_sync", "lshbloom_bands_begin", "lshbloom_bands_add", "lshbloom_bands_finish")
 
 
 def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
@@ -82,6 +82,9 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
               "lshbloom_query_insert", "lshbloom_query_insert_async"):
         getattr(lib, f).argtypes = [vp, ctypes.POINTER(_Batch), vp]
     lib.lshbloom_sync.argtypes = [vp]
+    lib.lshbloom_bands_begin.argtypes = [vp, u64]
+    lib.lshbloom_bands_add.argtypes = [vp, vp, u64, u64, vp]
+    lib.lshbloom_bands_finish.argtypes = [vp, vp, vp]
     lib.lshbloom_query_insert_bands.argtypes = [vp, vp, u64, i32, vp, vp]
     lib.lshbloom_reset.argtypes = [vp]
     lib.lshbloom_filter_copy.argtypes = [vp, u32, vp]
@@ -101,7 +104,7 @@ def load_library(path: str = _LIB_PATH) -> ctypes.CDLL:
     for f in EXPORTS:
         if f not in ("lshbloom_destroy", "lshbloom_last_error", "lshbloom_launch_count", "lshbloom_optimal_params", "lshbloom_plan",
            "lshbloom_band_hashes_to_peers", "lshbloom_query_insert_bands_peers", "lshbloom_query_insert_async",
-           "lshbloom_sync"):
+           "lshbloom_sync", "lshbloom_bands_begin", "lshbloom_bands_add", "lshbloom_bands_finish"):
             getattr(lib, f).restype = ctypes.c_int
     return lib
 
@@ -316,6 +319,37 @@ class LSHBloom:
             stream = torch.cuda.current_stream(bh_owned.device).cuda_stream
         self._check(self._lib.lshbloom_query_insert_bands(self._h, p, n, dev, stream or None,
                                                           self._ptr(out)))
+        return out
+
+    def bands_begin(self, n_global: int):
+        """Start a batch of n_global documents assembled from band-hash chunks."""
+        self._check(self._lib.lshbloom_bands_begin(self._h, int(n_global)))
+        self._bands_n = int(n_global)
+
+    def bands_add(self, bh_owned, doc0: int, *, stream=None):
+        """Add bh_owned [n][band_hi - band_lo] (device) for global documents [doc0, doc0 + n)."""
+        p, dev, keep = _raw(bh_owned, "bh_owned", 8)
+        if not dev:
+            raise ValueError("bh_owned must be a device tensor")
+        n = bh_owned.shape[0]
+        if n and tuple(bh_owned.shape) != (n, self.band_hi - self.band_lo):
+            raise ValueError("bh_owned must be [n][%d]" % (self.band_hi - self.band_lo))
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(bh_owned.device).cuda_stream
+        self._check(self._lib.lshbloom_bands_add(self._h, p, int(doc0), n, stream or None))
+
+    def bands_finish(self, *, out=None, device=None, stream=None):
+        """Hit flags [n_global] (uint8, device) of the assembled batch; mutates the filters."""
+        import torch
+        n = self._bands_n
+        if out is None:
+            out = torch.empty(n, dtype=torch.uint8, device=device if device is not None else "cuda:%d" % self.device)
+        else:
+            _check_out(out, n, 1, True)
+        if stream is None:
+            stream = torch.cuda.current_stream(out.device).cuda_stream
+        self._check(self._lib.lshbloom_bands_finish(self._h, out.data_ptr(), stream or None))
         return out
 
     def band_hashes_to_peers(self, offsets, tokens, global_doc0: int, peer_recv, *, stream=None):

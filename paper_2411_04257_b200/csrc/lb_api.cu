@@ -47,6 +47,15 @@ constexpr uint64_t kGenMax = (1ull << 22) - 1;
 // Counter-mode expansion R(seed, dom, i) (DESIGN R5).
 uint64_t R(uint64_t seed, uint64_t dom, uint64_t i) { return mix64(seed + kGamma * ((dom << 32) + i + 1)); }
 
+struct SweepPlan {
+  bool use = false;
+  uint32_t wb = 0, cap = 0;
+  uint64_t nw = 0, nbins = 0, piece = 0;
+  bool two_level = false;         // K7a + K7b (k = 17)
+  uint32_t cb = 0, ccap = 0;
+  uint64_t ncb = 0;
+};
+
 }  // namespace
 
 struct lshbloom {
@@ -97,6 +106,11 @@ struct lshbloom {
   std::string async_msg;
   cudaStream_t k1_stream1 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_pre = nullptr;
+  // a batch assembled from band-hash chunks (lshbloom_bands_begin / _add / _finish)
+  bool bands_open = false;
+  uint64_t bands_n = 0, bands_added = 0;
+  SweepPlan bands_plan;
+  DevBuf bands_bh;                // [bl][n_global] band-major
   uint64_t doc_count = 0, launches = 0;
   // classic MinHashLSH index (index_kind = LSHBLOOM_INDEX_CLASSIC)
   uint64_t* d_ckeys = nullptr;    // [bl][2^c_log2cap]
@@ -174,7 +188,7 @@ void free_all(lshbloom* h) {
   if (h->ev_pre) cudaEventDestroy(h->ev_pre);
   F(h->off.p); F(h->tok[0].p); F(h->tok[1].p); F(h->tok[2].p); F(h->bh.p); F(h->dup.p); F(h->sig.p); F(h->part.p);
   F(h->sw_cursor.p); F(h->sw_cursor2.p); F(h->sw_start.p); F(h->sw_rec.p); F(h->sw_miss.p); F(h->sw_eg.p);
-  F(h->sw_ccursor.p); F(h->sw_crec.p); F(h->sw_bht.p);
+  F(h->sw_ccursor.p); F(h->sw_crec.p); F(h->sw_bht.p); F(h->bands_bh.p);
   for (int i = 0; i < 3; i++) {
     if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
     if (h->ev_k1[i]) cudaEventDestroy(h->ev_k1[i]);
@@ -541,15 +555,6 @@ int run_bloom(lshbloom* h, const uint64_t* bh_dev, uint64_t bh_sj, uint64_t bh_s
 constexpr uint64_t kSweepMaxDocs = 1ull << 22;   // documents per sweep (records carry 32-bit
                                                  // document offsets; path (b) keeps 32-bit minima)
 
-struct SweepPlan {
-  bool use = false;
-  uint32_t wb = 0, cap = 0;
-  uint64_t nw = 0, nbins = 0, piece = 0;
-  bool two_level = false;         // K7a + K7b (k = 17)
-  uint32_t cb = 0, ccap = 0;
-  uint64_t ncb = 0;
-};
-
 // Bin capacity for an expected load of mu records: 7 standard deviations of a Poisson load, slack
 // for the band hashes near-duplicates share, and `pad` records of sector padding.
 // Rounded up to whole 32-byte sectors so that every bin starts sector-aligned.
@@ -563,10 +568,10 @@ uint32_t sweep_cap_for(double mu, double pad = 0.0) {
 // of the two-level binning (<= kSweepMaxCoarse per band, <= 512 windows each), and whether the
 // sweep beats random access (AUTO: owned filters beyond 96 MB, i.e. not L2-resident, and >= 256
 // probes per 64 KB window).
-SweepPlan plan_sweep(const lshbloom* h, uint64_t n) {
+SweepPlan plan_sweep(const lshbloom* h, uint64_t n, uint64_t max_piece = kSweepMaxDocs) {
   SweepPlan sp;
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC || h->bloom_path == LSHBLOOM_PATH_RANDOM || n == 0) return sp;
-  sp.piece = std::min<uint64_t>(n, kSweepMaxDocs);
+  sp.piece = std::min<uint64_t>(n, max_piece);
   const double rho = (double)sp.piece * h->k / (double)h->m;      // records per filter bit
   const double tiles = std::ceil((double)sp.piece / kSweepTileDocs);
   auto coarse = [&](uint32_t wb, uint32_t& cb, uint64_t& ncb, uint32_t& ccap) {
@@ -1357,6 +1362,87 @@ int lshbloom_query_insert_bands(lshbloom* h, const uint64_t* bh_owned, uint64_t 
   if (!on_device) LB_CUDA(h, cudaMemcpyAsync(hit_out, dhit, n_docs, cudaMemcpyDeviceToHost, s));
   if ((rc = finish(h, s))) return rc;
   h->doc_count += n_docs;
+  return LSHBLOOM_OK;
+}
+
+// ---- a batch of the owned bands assembled from band-hash chunks (pipelined sharded steps)
+int lshbloom_bands_begin(lshbloom* h, uint64_t n_global) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (n_global == 0 || n_global > 0xFFFFFFFFull) return fail(h, LSHBLOOM_EUSAGE, "n_global must be in [1, 2^32)");
+  if ((rc = classic_capacity(h, n_global))) return rc;
+  DeviceGuard g(h->device);
+  if ((rc = begin_sync(h))) return rc;
+  LB_CUDA(h, cudaStreamSynchronize(h->bloom_stream));
+  h->bands_plan = plan_sweep(h, n_global, n_global);          // one sweep over the whole batch
+  LB_CUDA(h, ensure(h->bands_bh, n_global * h->bl * sizeof(uint64_t)));
+  if (h->bands_plan.use) {
+    if ((rc = sweep_alloc(h, h->bands_plan, h->bloom_stream))) return rc;
+    const BloomParams bp = bloom_params(h, (const uint64_t*)h->bands_bh.p, n_global, 1, nullptr, nullptr);
+    if ((rc = sweep_begin(h, sweep_params(h, h->bands_plan, bp, 0, n_global), h->bloom_stream))) return rc;
+  }
+  if ((rc = reset_err(h, h->bloom_stream))) return rc;
+  h->bands_open = true;
+  h->bands_n = n_global;
+  h->bands_added = 0;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_bands_add(lshbloom* h, const uint64_t* bh_owned, uint64_t doc0, uint64_t n_docs, void* stream) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->bands_open) return fail(h, LSHBLOOM_EUSAGE, "lshbloom_bands_add without lshbloom_bands_begin");
+  if (n_docs == 0) return LSHBLOOM_OK;
+  if (!bh_owned) return fail(h, LSHBLOOM_EUSAGE, "NULL bh_owned");
+  if (doc0 > h->bands_n || n_docs > h->bands_n - doc0) return fail(h, LSHBLOOM_EUSAGE, "chunk beyond n_global");
+  DeviceGuard g(h->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
+  const uint64_t n = h->bands_n;
+  // the chunk is copied (transposed) into the batch's band-major buffer on the Bloom stream, after
+  // the caller's stream has produced it; the caller may reuse it once its stream passes ev_fuse
+  LB_CUDA(h, cudaEventRecord(h->ev_in, s));
+  LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_in, 0));
+  h->launches += launch_transpose_bh(bh_owned, (uint64_t*)h->bands_bh.p, (uint32_t)n_docs, h->bl, h->bloom_stream, n,
+                                     doc0);
+  if (h->bands_plan.use) {                                     // bin this chunk's probes now
+    const BloomParams bp = bloom_params(h, (const uint64_t*)h->bands_bh.p, n, 1, nullptr, nullptr);
+    if ((rc = sweep_bin(h, sweep_params(h, h->bands_plan, bp, 0, n), doc0, doc0 + n_docs, h->bloom_stream))) return rc;
+  }
+  LB_CUDA(h, cudaEventRecord(h->ev_fuse, h->bloom_stream));
+  LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_fuse, 0));
+  LB_CUDA(h, cudaGetLastError());
+  h->bands_added += n_docs;
+  return LSHBLOOM_OK;
+}
+
+int lshbloom_bands_finish(lshbloom* h, uint8_t* hit_out, void* stream) {
+  int rc = check_handle(h);
+  if (rc) return rc;
+  if (!h->bands_open) return fail(h, LSHBLOOM_EUSAGE, "lshbloom_bands_finish without lshbloom_bands_begin");
+  if (!hit_out) return fail(h, LSHBLOOM_EUSAGE, "NULL hit_out");
+  h->bands_open = false;
+  if (h->bands_added != h->bands_n)
+    return fail(h, LSHBLOOM_EUSAGE, "lshbloom_bands_add covered " + std::to_string(h->bands_added) + " of " +
+                                        std::to_string(h->bands_n) + " documents");
+  DeviceGuard g(h->device);
+  cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
+  const uint64_t n = h->bands_n;
+  LB_CUDA(h, cudaEventRecord(h->ev_in, s));
+  LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_in, 0));
+  LB_CUDA(h, cudaMemsetAsync(hit_out, 0, n, h->bloom_stream));
+  const uint64_t* bh = (const uint64_t*)h->bands_bh.p;
+  if (h->bands_plan.use) {
+    const BloomParams bp = bloom_params(h, bh, n, 1, hit_out, nullptr);
+    stage_begin(h, 1, h->bloom_stream);
+    if ((rc = sweep_finish(h, sweep_params(h, h->bands_plan, bp, 0, n), h->bloom_stream, true, true))) return rc;
+    stage_end(h, 1, h->bloom_stream);
+  } else if ((rc = run_bloom(h, bh, n, 1, 0, n, hit_out, h->bloom_stream))) {
+    return rc;
+  }
+  LB_CUDA(h, cudaEventRecord(h->ev_fuse, h->bloom_stream));
+  LB_CUDA(h, cudaStreamWaitEvent(s, h->ev_fuse, 0));
+  if ((rc = finish(h, h->bloom_stream))) return rc;
+  h->doc_count += n;
   return LSHBLOOM_OK;
 }
 

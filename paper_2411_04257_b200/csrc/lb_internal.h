@@ -167,7 +167,9 @@ int launch_sweep_finish(const SweepParams& p, int grid, cudaStream_t s);
 struct SweepLaunch { int grid; uint32_t stages; size_t smem; };
 SweepLaunch sweep_launch_cfg(int sm_count, uint32_t wb);   // K8 persistent grid / pipeline depth
 int sweep_grid(int sm_count, uint32_t wb);                 // = sweep_launch_cfg().grid
-int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t bl, cudaStream_t s);
+// [n][bl] -> columns [col0, col0 + n) of a [bl][ld] buffer (ld = 0: ld = n)
+int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t bl, cudaStream_t s,
+                        uint64_t ld = 0, uint64_t col0 = 0);
 constexpr int kSweepThreads = 256;               // K8 block size
 constexpr int kSweepRPT = 4;                     // records per thread held in registers
 constexpr uint32_t kSweepCapReg = kSweepThreads * kSweepRPT;   // 1024: larger bins take the global path

@@ -412,9 +412,10 @@ __global__ void __launch_bounds__(SW_BIN_THREADS) kf_count(const SweepParams p, 
   }
 }
 
-// Band hashes [n][bl] (row-major, query_insert_bands) -> [bl][n] (band-major), so that the
-// binning kernels read them coalesced.
-__global__ void k7_transpose(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint32_t n, uint32_t bl) {
+// Band hashes [n][bl] (row-major, query_insert_bands) -> columns [col0, col0 + n) of a band-major
+// [bl][ld] buffer, so that the binning kernels read them coalesced.
+__global__ void k7_transpose(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint32_t n, uint32_t bl,
+                             uint64_t ld, uint64_t col0) {
   __shared__ uint64_t t[32][33];
   const uint32_t d0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
   for (uint32_t y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -424,12 +425,13 @@ __global__ void k7_transpose(const uint64_t* __restrict__ in, uint64_t* __restri
   __syncthreads();
   for (uint32_t y = threadIdx.y; y < 32; y += blockDim.y) {
     const uint32_t j = j0 + y, d = d0 + threadIdx.x;
-    if (d < n && j < bl) out[(uint64_t)j * n + d] = t[threadIdx.x][y];
+    if (d < n && j < bl) out[(uint64_t)j * ld + col0 + d] = t[threadIdx.x][y];
   }
 }
 
-int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t bl, cudaStream_t s) {
-  k7_transpose<<<dim3((n + 31) / 32, (bl + 31) / 32), dim3(32, 8), 0, s>>>(in, out, n, bl);
+int launch_transpose_bh(const uint64_t* in, uint64_t* out, uint32_t n, uint32_t bl, cudaStream_t s,
+                        uint64_t ld, uint64_t col0) {
+  k7_transpose<<<dim3((n + 31) / 32, (bl + 31) / 32), dim3(32, 8), 0, s>>>(in, out, n, bl, ld ? ld : n, col0);
   return 1;
 }
 

@@ -14,6 +14,14 @@ Per batch:
 Results are bit-identical for every world size.  The collectives are plumbing (torch /
 NCCL); every arithmetic step runs in the library's kernels.
 
+With the NCCL exchange the step is pipelined over chunks of `pipeline_docs` local documents
+(default 262144): chunk c's band hashes are exchanged (one all_to_all per chunk) and handed to
+the owners' engines (lshbloom_bands_add: copied into the batch and, with the window sweep,
+binned at once) while every rank computes chunk c+1's MinHash; the query-then-insert runs once
+per batch (lshbloom_bands_finish) over the whole global batch in stream order = rank order, so
+the flags do not depend on the world size or the chunk size.  pipeline_docs=0 exchanges the
+batch in one piece (steps 1-4 above).
+
 exchange="p2p" replaces steps 1-4 by stores into peer memory: K1's
 epilogue writes every band hash straight into its owner's receive buffer (torch symmetric
 memory over NVLink / NVSwitch; lshbloom_band_hashes_to_peers), and the Bloom kernels raise each
@@ -22,6 +30,7 @@ with three device-side barriers per batch and no all-to-all, all-reduce or pack 
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -36,10 +45,11 @@ def band_range(rank: int, world: int, b: int) -> tuple[int, int]:
 class ShardedLSHBloom:
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, group=None, device: int | None = None, sub_batch: int = 0, index: str = "bloom",
-                 exchange: str = "nccl", engine=None):
+                 exchange: str = "nccl", engine=None, pipeline_docs: int = 262144):
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
         self.exchange = exchange
+        self.pipeline_docs = int(pipeline_docs)
         self._p2p = None
         self.group = group
         self.rank = dist.get_rank(group)
@@ -69,6 +79,8 @@ class ShardedLSHBloom:
         counts = self._counts(n_local, device)
         if self.exchange == "p2p":
             return self._query_insert_p2p(offsets, tokens, counts, device)
+        if self.pipeline_docs > 0:
+            return self._query_insert_pipelined(offsets, tokens, counts, device)
         if n_local:
             send = self.engine.band_hashes_sharded(offsets, tokens)      # owner-major, flat
         else:                                                            # this rank has no documents
@@ -82,6 +94,39 @@ class ShardedLSHBloom:
         dist.all_reduce(hits, op=dist.ReduceOp.MAX, group=self.group)
         start = sum(counts[:self.rank])
         return hits[start:start + n_local]
+
+    def _query_insert_pipelined(self, offsets, tokens, counts, device):
+        n_local = counts[self.rank]
+        n_global = sum(counts)
+        starts = [0]
+        for c in counts:
+            starts.append(starts[-1] + c)
+        C = self.pipeline_docs
+        nchunks = max(1, -(-max(counts) // C))
+        off_h = offsets.cpu().numpy().view(np.uint64) if n_local else None   # chunk bounds (one copy)
+        self.engine.bands_begin(n_global)
+        for c in range(nchunks):
+            a, b = min(c * C, n_local), min((c + 1) * C, n_local)
+            if b > a:
+                o = torch.from_numpy((off_h[a:b + 1] - off_h[a]).view(np.int64)).to(device, non_blocking=True)
+                t = tokens[int(off_h[a]):int(off_h[b])]
+                send = self.engine.band_hashes_sharded(o, t)             # owner-major, flat
+            else:
+                send = torch.empty(0, dtype=torch.int64, device=device)
+            part = [max(0, min(C, counts[r] - c * C)) for r in range(self.world)]
+            in_splits = [(b - a) * w for w in self.widths]
+            out_splits = [k * self.bl for k in part]
+            recv = torch.empty(sum(out_splits), dtype=torch.int64, device=device)
+            dist.all_to_all_single(recv, send, out_splits, in_splits, group=self.group)
+            pos = 0
+            for r in range(self.world):                                 # rank r's chunk c, in place
+                if part[r]:
+                    self.engine.bands_add(recv[pos:pos + part[r] * self.bl].view(part[r], self.bl),
+                                          starts[r] + c * C)
+                pos += part[r] * self.bl
+        hits = self.engine.bands_finish(device=device)
+        dist.all_reduce(hits, op=dist.ReduceOp.MAX, group=self.group)
+        return hits[starts[self.rank]:starts[self.rank] + n_local]
 
     def reset(self):
         self.engine.reset()

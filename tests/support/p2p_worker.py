@@ -17,6 +17,9 @@ from synthetic.corpus import CONFIGS, gen_range  # noqa: E402
 
 def main():
     exchange = sys.argv[1] if len(sys.argv) > 1 else "p2p"
+    pipeline = 262144
+    if ":" in exchange:                      # "nccl:<pipeline_docs>"
+        exchange, pipeline = exchange.split(":")[0], int(exchange.split(":")[1])
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
@@ -26,7 +29,7 @@ def main():
     per = 2500
     batches = [(0, per * world), (per * world, per * world + 777 * world)]
     sx = ShardedLSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=local,
-                         exchange=exchange)
+                         exchange=exchange, pipeline_docs=pipeline)
     ok = True
     ref = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=local) if rank == 0 else None
     for a, c in batches:

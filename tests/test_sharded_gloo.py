@@ -40,6 +40,21 @@ class OracleEngine:
         dup = self.index.query_insert(bh_owned.numpy().view(np.uint64), band_lo=self.band_lo, nthreads=2)
         return torch.from_numpy(dup)
 
+    # pipelined form (lshbloom_bands_begin / _add / _finish)
+    def bands_begin(self, n_global):
+        self._rows = np.full((n_global, self.band_hi - self.band_lo), -1, np.int64)
+        self._seen = np.zeros(n_global, bool)
+
+    def bands_add(self, bh_owned, doc0):
+        n = bh_owned.shape[0]
+        assert not self._seen[doc0:doc0 + n].any()          # every document exactly once
+        self._rows[doc0:doc0 + n] = bh_owned.numpy()
+        self._seen[doc0:doc0 + n] = True
+
+    def bands_finish(self, device=None):
+        assert self._seen.all()
+        return self.query_insert_bands(torch.from_numpy(self._rows))
+
     def reset(self):
         pass
 
@@ -52,12 +67,13 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cuts, n_total, out_path):
+def _worker(rank, world, port, cuts, n_total, out_path, pipeline_docs=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     cfg = CONFIGS["C1"]
-    sx = ShardedLSHBloom(NP, B, R, n_total, FP, SEED, engine=OracleEngine(rank, world, n_total))
+    sx = ShardedLSHBloom(NP, B, R, n_total, FP, SEED, engine=OracleEngine(rank, world, n_total),
+                         pipeline_docs=pipeline_docs)
     flags = []
     for batch in cuts:                       # several batches: filter state persists across calls
         a, b = batch[rank], batch[rank + 1]
@@ -69,8 +85,8 @@ def _worker(rank, world, port, cuts, n_total, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_flags_equal_single_process_oracle(world, tmp_path):
+@pytest.mark.parametrize("world,pipeline_docs", [(2, 0), (3, 0), (2, 97), (3, 500), (3, 1 << 18)])
+def test_sharded_flags_equal_single_process_oracle(world, pipeline_docs, tmp_path):
     # two stream batches; each split into `world` unequal contiguous rank shards
     rng = np.random.default_rng(world)
     bounds = [0, 1400, 1401, 3000]                       # includes a one-document batch
@@ -82,7 +98,7 @@ def test_sharded_flags_equal_single_process_oracle(world, tmp_path):
         inner = sorted(rng.choice(np.arange(a + 1, b), world - 1, replace=False).tolist())
         cuts.append([a] + inner + [b])
     out = str(tmp_path / "flags_%d.npy")
-    mp.spawn(_worker, args=(world, _free_port(), cuts, bounds[-1], out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cuts, bounds[-1], out, pipeline_docs), nprocs=world, join=True)
     got = []
     per_rank = [np.load(out % r) for r in range(world)]
     # reassemble global order: batch by batch, rank by rank
