@@ -350,6 +350,7 @@ def c5_leg(args, torch, dev, peaks, peak_src):
                                                      device=dev.index), bhs, probes, peaks, peak_src, steps)
     tr = load_json("bloom_sweep_traffic_C5.json")
     alone["traffic"] = tr["dram_bytes_per_probe"] * probes if tr else None
+    alone["traffic_source"] = "profiles/bloom_sweep_traffic_C5.json (ncu, same batch shape)" if tr else None
     del bhs
     torch.cuda.empty_cache()
     return {"workload": "C5 geometry: 128 perms, b=20 r=6, n_expected=1e9 (%.1f GB of filters, m=%d > 2^32), "
