@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>   // CUstream / CUdeviceptr types for the stream memory operation (no -lcuda)
+
 #include "../../include/lshbloom.h"
 #include "lb_internal.h"
 
@@ -64,6 +66,7 @@ struct lshbloom {
   uint64_t nb = 0, nb_inv = 0;    // blocked variant: 1024-bit blocks per band
   uint32_t k = 0, band_lo = 0, band_hi = 0, bl = 0, npl = 0, sub_batch = 0;
   int device = 0, sm_count = 148;
+  size_t total_mem = 0;
   cudaStream_t own_stream = nullptr, copy_stream = nullptr, bloom_stream = nullptr;
   cudaStream_t k1_stream2 = nullptr, k1_stream3 = nullptr;  // fused step: K1 chunks round-robin, a chunk's tail overlaps the next
   cudaEvent_t ev_fuse = nullptr, ev_join = nullptr, ev_join3 = nullptr;
@@ -99,6 +102,12 @@ struct lshbloom {
     uint64_t n = 0, seq = 0;
     cudaEvent_t done = nullptr;
     DevBuf bh, off, dup;
+    // landing-gated host batches: the whole token array lands here while K1 runs; *landed counts
+    // landed pieces (written by cuStreamWriteValue32 on the copy stream); tok_free is recorded
+    // when the batch's last K1 launch is done (the next copy into this buffer waits for it)
+    DevBuf tokall;
+    uint32_t* landed = nullptr;
+    cudaEvent_t tok_free = nullptr;
   } slot[2];
   int next_slot = 0;
   uint64_t seq = 0;
@@ -106,6 +115,11 @@ struct lshbloom {
   std::string async_msg;
   cudaStream_t k1_stream1 = nullptr;
   cudaEvent_t ev_in = nullptr, ev_pre = nullptr;
+  // cuStreamWriteValue32 (driver entry point, resolved at create; null: host batches use the
+  // staging path) and the landing piece, 2^land_log2 tokens
+  CUresult (*write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  uint32_t land_log2 = 21;
+  bool land_enabled = true;
   // a batch assembled from band-hash chunks (lshbloom_bands_begin / _add / _finish)
   bool bands_open = false;
   uint64_t bands_n = 0, bands_added = 0;
@@ -180,8 +194,9 @@ void free_all(lshbloom* h) {
   F(h->d_coef); F(h->d_bcoef); F(h->d_s1); F(h->d_s2); F(h->d_F); F(h->d_Q); F(h->d_clist); F(h->d_cb); F(h->d_ekey);
   F(h->d_eval); F(h->d_st); F(h->d_ckeys); F(h->d_cvals); F(h->d_cand); F(h->d_counters); F(h->d_err_base);
   for (auto& sl : h->slot) {
-    F(sl.bh.p); F(sl.off.p); F(sl.dup.p);
+    F(sl.bh.p); F(sl.off.p); F(sl.dup.p); F(sl.tokall.p); F(sl.landed);
     if (sl.done) cudaEventDestroy(sl.done);
+    if (sl.tok_free) cudaEventDestroy(sl.tok_free);
   }
   if (h->k1_stream1) cudaStreamDestroy(h->k1_stream1);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
@@ -204,6 +219,34 @@ void free_all(lshbloom* h) {
   if (h->bloom_stream) cudaStreamDestroy(h->bloom_stream);
   if (h->own_stream) cudaStreamDestroy(h->own_stream);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+}
+
+// Landing-gated host batches (MinhashParams::landed): resolve cuStreamWriteValue32 through the
+// runtime's driver entry point (no link against libcuda) and check once that a stream write
+// lands; otherwise host batches keep the staging path.  LSHBLOOM_LANDING=0 disables the gate,
+// LSHBLOOM_LAND_LOG2 sets the landing piece (2^k tokens, 18..28; default 2^21 = 8 MB: C3 e2e 106.4 / 106.9 / 108.0 ms per 200K documents at 2^21 / 2^23 / 2^25).
+void init_landing(lshbloom* h) {
+  h->write_value32 = nullptr;
+  if (const char* e = getenv("LSHBLOOM_LANDING")) h->land_enabled = atoi(e) != 0;
+  if (const char* e = getenv("LSHBLOOM_LAND_LOG2")) h->land_log2 = (uint32_t)std::min(28, std::max(18, atoi(e)));
+  if (!h->land_enabled) return;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return;
+  }
+  auto wv = (CUresult(*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int))fn;
+  uint32_t got = 0;
+  if (wv((CUstream)h->own_stream, (CUdeviceptr)h->slot[0].landed, 0x1A2B3C4Du, 0) != CUDA_SUCCESS ||
+      cudaMemcpyAsync(&got, h->slot[0].landed, 4, cudaMemcpyDeviceToHost, h->own_stream) != cudaSuccess ||
+      cudaStreamSynchronize(h->own_stream) != cudaSuccess || got != 0x1A2B3C4Du) {
+    cudaGetLastError();
+    return;
+  }
+  cudaMemset(h->slot[0].landed, 0, 4);
+  h->write_value32 = wv;
 }
 
 // Host-side CSR validation; returns 0, 1 (usage) or 2 (empty doc).
@@ -258,9 +301,10 @@ int collect(lshbloom* h, int si) {
   if (e.flags || e.first_empty != ~0ull) {
     h->doc_count -= std::min(h->doc_count, sl.n);
     if (!h->async_rc) {
-      h->async_rc = e.flags ? LSHBLOOM_EUSAGE : LSHBLOOM_EDATA;
-      h->async_msg = e.flags ? "malformed offsets (offsets[0] != 0 or decreasing)"
-                             : "empty document at index " + std::to_string(e.first_empty);
+      h->async_rc = (e.flags & 2) ? LSHBLOOM_ERUNTIME : e.flags ? LSHBLOOM_EUSAGE : LSHBLOOM_EDATA;
+      h->async_msg = (e.flags & 2) ? "timed out waiting for the batch's tokens to land in device memory"
+                     : e.flags ? "malformed offsets (offsets[0] != 0 or decreasing)"
+                               : "empty document at index " + std::to_string(e.first_empty);
     }
   }
   return LSHBLOOM_OK;
@@ -372,9 +416,10 @@ int run_minhash(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, uint32_t* 
   const uint64_t n = b->n_docs;
   MinhashParams p = base_params(h);
   if (h->npl >= 8) {   // scratch of the length-partitioned K1 launches (lb_minhash.cu)
-    LB_CUDA(h, ensure(h->part, (2 * (size_t)b->n_docs + 2) * sizeof(uint32_t)));
+    LB_CUDA(h, ensure(h->part, (2 * (size_t)b->n_docs + 2 + b->n_docs / 1024 + 1) * sizeof(uint32_t)));
     p.part_lists = (uint32_t*)h->part.p;
     p.part_counts = (uint32_t*)h->part.p + 2 * b->n_docs;
+    p.part_blk = p.part_counts + 2;
   }
   p.sig_out = sig_dev;
   p.bh_out = bh_dev;
@@ -797,13 +842,22 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
   uint64_t* bh = (uint64_t*)sl.bh.p;
   MinhashParams p = base_params(h);
   if (h->npl >= 8) {   // scratch of the length-partitioned K1 launches (lb_minhash.cu), per K1 stream
-    int rc0 = grow(h, h->part, (6 * (size_t)b->n_docs + 6) * sizeof(uint32_t));
+    int rc0 = grow(h, h->part, (6 * (size_t)b->n_docs + 6 + 3 * (b->n_docs / 1024 + 1)) * sizeof(uint32_t));
     if (rc0) return rc0;
   }
   p.bh_out = bh;
   p.map = resolve_map(owned_band_major_map(h, n), bh, h->cfg.b);
   const uint64_t chunk_tokens = b->on_device ? 0 : kChunkTokens;
   if (!b->on_device && b->offsets[0] != 0) return fail(h, LSHBLOOM_EUSAGE, "offsets[0] must be 0");
+  // Landing-gated host batch: the whole token array is copied into the slot's device buffer in
+  // 2^land_log2-token pieces on the copy stream while K1 runs over it in the device-resident
+  // chunking, each warp waiting only for its own document's tokens (MinhashParams::landed):
+  // no staging-sized K1 chunks, no tails per staging buffer.  Needs the stream write and a
+  // buffer of the batch's size (at most 1/8 of device memory); otherwise the staging path.
+  const uint64_t n_tok_host = b->on_device ? 0 : b->offsets[n];
+  const bool landing = !b->on_device && h->write_value32 &&
+                       n_tok_host * sizeof(uint32_t) <= h->total_mem / 8;
+  const bool dev_chunks = b->on_device || landing;
   // Bloom path: with the sweep, each chunk's probes are binned right after its K1 (overlapping
   // the next chunk's K1) and every piece of <= kSweepMaxDocs documents is swept once complete;
   // chunk boundaries fall on piece boundaries.
@@ -818,7 +872,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
   // (host batches keep their staging-sized chunks: those overlap the H2D copy with K1)
   auto clip = [&](uint64_t d0, uint64_t d1) {
     if (!sp.use) return d1;
-    if (b->on_device) d1 = std::max(d1, std::min(n, d0 + sweep_chunk));
+    if (dev_chunks) d1 = std::max(d1, std::min(n, d0 + sweep_chunk));
     return std::min(d1, (d0 / kSweepMaxDocs + 1) * kSweepMaxDocs);
   };
   // Chunk bounds first, all of them checked before anything is enqueued: a host batch's copies
@@ -830,8 +884,11 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
     uint64_t d0 = 0;
     while (d0 < n) {
       uint64_t d1;
-      if (b->on_device) {
+      if (dev_chunks) {
         d1 = clip(d0, fuse_chunk_end(d0, n, h->npl));
+        if (landing && (b->offsets[d1] < b->offsets[d0] || b->offsets[d1] > n_tok_host))
+          return fail(h, LSHBLOOM_EUSAGE, "malformed offsets near index " + std::to_string(d0) +
+                                              " (decreasing, or beyond offsets[n_docs])");
       } else {
         const uint64_t t0 = b->offsets[d0];
         const uint64_t* lim = std::upper_bound(b->offsets + d0 + 1, b->offsets + n + 1, t0 + chunk_tokens);
@@ -884,16 +941,48 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
     LB_CUDA(h, ensure(sl.off, (n + 1) * sizeof(uint64_t)));
     LB_CUDA(h, cudaMemcpyAsync(sl.off.p, b->offsets, (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, s0));
     h->launches += launch_validate((const uint64_t*)sl.off.p, n, h->d_err, s0);
-    nbuf = host_bufs(n, b->offsets[n]);
-    const uint64_t buf_tokens = std::max<uint64_t>(1, std::min(chunk_tokens, b->offsets[n]));
-    for (int i = 0; i < nbuf; i++)
-      if (buf_tokens * sizeof(uint32_t) > h->tok[i].cap) {
-        LB_CUDA(h, cudaEventSynchronize(h->ev_k1[i]));     // its last reader is done
-        LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
-      }
     p.offsets = (const uint64_t*)sl.off.p;
+    if (landing) {
+      LB_CUDA(h, ensure(sl.tokall, n_tok_host * sizeof(uint32_t)));   // (the slot is idle: collected)
+      LB_CUDA(h, cudaMemsetAsync(sl.landed, 0, 4, s0));
+      p.tokens = (const uint32_t*)sl.tokall.p;
+      p.tok_base = 0;
+      p.landed = sl.landed;
+      p.land_log2 = h->land_log2;
+      p.tok_total = n_tok_host;
+      p.err_state = h->d_err;
+    } else {
+      nbuf = host_bufs(n, b->offsets[n]);
+      const uint64_t buf_tokens = std::max<uint64_t>(1, std::min(chunk_tokens, b->offsets[n]));
+      for (int i = 0; i < nbuf; i++)
+        if (buf_tokens * sizeof(uint32_t) > h->tok[i].cap) {
+          LB_CUDA(h, cudaEventSynchronize(h->ev_k1[i]));     // its last reader is done
+          LB_CUDA(h, ensure(h->tok[i], buf_tokens * sizeof(uint32_t)));
+        }
+    }
   }
   LB_CUDA(h, cudaEventRecord(h->ev_pre, s0));               // error gate and offsets ready
+  if (landing) {
+    // every piece and its landing mark are enqueued before any K1 launch, so a waiting warp
+    // only ever waits on copy-engine work (no SM involved); the copies start once the slot's
+    // previous K1 reader is done and this batch's landing counter is zeroed
+    LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_pre, 0));
+    LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, sl.tok_free, 0));
+    const uint64_t piece = 1ull << h->land_log2;
+    uint32_t i = 0;
+    for (uint64_t t0 = 0; t0 < n_tok_host; t0 += piece) {
+      const uint64_t t1 = std::min(n_tok_host, t0 + piece);
+      LB_CUDA(h, cudaMemcpyAsync((uint32_t*)sl.tokall.p + t0, b->tokens + t0, (t1 - t0) * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, h->copy_stream));
+      if (h->write_value32((CUstream)h->copy_stream, (CUdeviceptr)sl.landed, ++i, 0) != CUDA_SUCCESS)
+        return fail(h, LSHBLOOM_ERUNTIME, "cuStreamWriteValue32 failed");
+    }
+    static const bool land_diag = [] { const char* e = getenv("LSHBLOOM_LAND_DIAG"); return e && atoi(e); }();
+    if (land_diag) {   // diagnostic: K1 starts only after the whole copy (no overlap)
+      LB_CUDA(h, cudaEventRecord(h->ev_h2d[0], h->copy_stream));
+      for (int k = 0; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_h2d[0], 0));
+    }
+  }
   for (int k = 1; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_pre, 0));
   LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_pre, 0));
   LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, h->bloom_stream));
@@ -901,7 +990,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
   stage_begin(h, 0, s0);
   for (const auto& ch : chunks) {
     const uint64_t d0 = ch.first, d1 = ch.second;
-    if (!b->on_device) {
+    if (!dev_chunks) {
       const uint64_t t0 = b->offsets[d0], t1 = b->offsets[d1];
       const int buf = c % nbuf;
       if ((t1 - t0) * sizeof(uint32_t) > h->tok[buf].cap) {   // a chunk larger than the buffer
@@ -924,13 +1013,14 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
     if (h->npl >= 8) {
       p.part_lists = (uint32_t*)h->part.p + (size_t)par * 2 * n;
       p.part_counts = (uint32_t*)h->part.p + 6 * n + 2 * par;
+      p.part_blk = (uint32_t*)h->part.p + 6 * n + 6 + (size_t)par * (n / 1024 + 1);
     }
     LB_CUDA(h, cudaMemsetAsync(p.counter, 0, 4, ks));
     int l = launch_minhash(p, (int)h->npl, h->sm_count, ks, h->k1_bps);
     if (l < 0) return fail(h, LSHBLOOM_EUSAGE, "unsupported num_perm");
     h->launches += l;
     LB_CUDA(h, cudaGetLastError());
-    if (!b->on_device) LB_CUDA(h, cudaEventRecord(h->ev_k1[c % nbuf], ks));
+    if (!dev_chunks) LB_CUDA(h, cudaEventRecord(h->ev_k1[c % nbuf], ks));
     LB_CUDA(h, cudaEventRecord(h->ev_fuse, ks));
     if (d1 == n) {   // every K1 stream joined into the first before the stage's end mark
       cudaEvent_t ej[3] = {nullptr, h->ev_join, h->ev_join3};
@@ -939,6 +1029,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
         LB_CUDA(h, cudaStreamWaitEvent(s0, ej[k], 0));
       }
       stage_end(h, 0, s0);
+      if (landing) LB_CUDA(h, cudaEventRecord(sl.tok_free, s0));
     }
     LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_fuse, 0));
     if (!sp.use) {
@@ -1072,6 +1163,10 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
     }                                                \
   } while (0)
   CR(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, dev));
+  {
+    size_t fr = 0;
+    CR(cudaMemGetInfo(&fr, &h->total_mem));
+  }
   CR(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
   CR(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
   {
@@ -1089,7 +1184,13 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   CR(cudaStreamCreateWithFlags(&h->k1_stream1, cudaStreamNonBlocking));
   CR(cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming));
   CR(cudaEventCreateWithFlags(&h->ev_pre, cudaEventDisableTiming));
-  for (auto& sl : h->slot) CR(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+  for (auto& sl : h->slot) {
+    CR(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    CR(cudaEventCreateWithFlags(&sl.tok_free, cudaEventDisableTiming));
+    CR(cudaMalloc(&sl.landed, 4));
+    CR(cudaMemset(sl.landed, 0, 4));
+  }
+  init_landing(h);
   if (const char* e = getenv("LSHBLOOM_K1_STREAMS")) h->k1_nstreams = std::min(3, std::max(1, atoi(e)));
   if (const char* e = getenv("LSHBLOOM_K1_ALT")) h->k1_alt = atoi(e) != 0;
   h->k1_bps = 4;   // leave room on every SM for the concurrent Bloom kernels
@@ -1286,8 +1387,9 @@ static int enqueue_query_insert(lshbloom* h, const lshbloom_batch* b, uint8_t* d
   }
   if ((rc = run_query_insert(h, b, s, si, ddup, b->on_device ? nullptr : dup_out))) {
     // nothing of this batch can have mutated the filters (its K0 gate or a host check failed
-    // before any launch), but kernels may be queued: let them finish before returning
-    cudaStreamSynchronize(h->bloom_stream);
+    // before any launch), but kernels and copies may be queued: let them finish before returning
+    for (cudaStream_t q : {h->k1_stream1, h->k1_stream2, h->k1_stream3, h->copy_stream, h->bloom_stream})
+      cudaStreamSynchronize(q);
     return rc;
   }
   sl.busy = true;

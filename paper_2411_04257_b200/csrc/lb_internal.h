@@ -49,6 +49,12 @@ __device__ __forceinline__ void raise_dup(const DupSink& d, uint32_t i) {
   d.peer[lo][i - d.start[lo]] = 1;
 }
 
+struct ErrState {
+  int flags;                 // bit0: usage (offsets[0] != 0 or decreasing); bit1: landing-gate timeout
+  int pad;
+  unsigned long long first_empty;  // first empty document (~0 if none)
+};
+
 struct MinhashParams {
   const uint64_t* offsets;   // batch offsets (device), n+1
   const uint32_t* tokens;    // device tokens; document d starts at tokens[offsets[d] - tok_base]
@@ -73,7 +79,19 @@ struct MinhashParams {
   const uint32_t* list_n;
   uint32_t* part_lists;      // [2][n_docs]: short documents, long documents
   uint32_t* part_counts;     // [2]
+  uint32_t* part_blk;        // [ceil(n_docs / 1024)]: long documents per partition block
   uint32_t block_gate;       // screened kernel: block-per-document mode iff *list_n < block_gate
+  // Landing gate (host batches streamed into one device token buffer while K1 runs): the copy
+  // engine lands the tokens in pieces of 2^land_log2 tokens, in order, and after piece i a
+  // stream memory operation (no SM involved) writes *landed = i + 1.  A warp starts document d
+  // only when every 128-B line it can touch has landed -- tokens [0, roundup32(offsets[d+1]))
+  // clipped to tok_total -- so no SM ever caches a line that is still being written.  Null:
+  // the tokens are resident.  A wait beyond kLandTimeoutNs sets err_state->flags bit 1 and the
+  // gate (the batch is rejected with LSHBLOOM_ECUDA instead of hanging the device).
+  const uint32_t* landed;
+  uint32_t land_log2;
+  uint64_t tok_total;
+  ErrState* err_state;
 };
 
 struct BloomParams {
@@ -149,12 +167,6 @@ struct ClassicParams {        // classic MinHashLSH index (lb_classic.cu)
   DupSink dup;               // [batch] flags (OR over owned bands), local or in peer memory
   int* full;                 // set if a probe sequence wrapped (cannot happen at load <= 0.9)
   const int* err;
-};
-
-struct ErrState {
-  int flags;                 // bit0: usage (offsets[0] != 0 or decreasing)
-  int pad;
-  unsigned long long first_empty;  // first empty document (~0 if none)
 };
 
 // launchers (return number of kernel launches issued)

@@ -122,6 +122,48 @@ __device__ __forceinline__ uint32_t ld_token(const uint32_t* ptr, uint64_t pol) 
   return v;
 }
 
+// Landing gate (MinhashParams::landed): called by one thread for document d (token end o1)
+// before any lane reads the document.  Returns false if the tokens did not land within
+// kLandTimeoutNs (the batch is then rejected; see MinhashParams).
+constexpr uint64_t kLandTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool await_tokens_impl(const uint32_t* landed, uint32_t land_log2, uint64_t tok_total,
+                                              const int* gate, ErrState* es, uint64_t o1) {
+  const uint64_t r32 = (o1 + 31) & ~(uint64_t)31, end = tok_total < r32 ? tok_total : r32;
+  const uint32_t need = (uint32_t)((end + (1ull << land_log2) - 1) >> land_log2);
+  if (ld_acquire_u32(landed) >= need) return true;
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    __nanosleep(256);
+    if (ld_acquire_u32(landed) >= need) return true;
+    if (*(volatile const int*)gate) return false;             // the batch was rejected meanwhile
+    if (globaltimer_ns() - t0 > kLandTimeoutNs) {
+      atomicOr(&es->flags, 2);
+      atomicExch(&es->pad, 1);
+      return false;
+    }
+  }
+}
+__device__ __forceinline__ bool await_tokens(const MinhashParams& p, uint64_t o1) {
+  return await_tokens_impl(p.landed, p.land_log2, p.tok_total, p.err, p.err_state, o1);
+}
+// Per-warp form: lane 0 waits, the verdict is broadcast.
+__device__ __forceinline__ bool warp_await_tokens(const MinhashParams& p, uint32_t d, int lane) {
+  if (!p.landed) return true;
+  int ok = 1;
+  if (lane == 0) ok = await_tokens(p, p.offsets[d + 1]);
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
   uint64_t x = mod_p(fp);
   XLimbs l;
@@ -137,7 +179,7 @@ __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
 // shared memory for the band hashes): the register footprint of NPL permutations per lane for
 // PASSES x NPL of them -- 256 permutations on short documents at 4 per lane run at the 128-
 // permutation kernel's occupancy instead of the 8-per-lane kernel's.
-template <int NPL, int UNR, int MINB = LB_K1_MINB, int PASSES = 1>
+template <int NPL, int UNR, int MINB = LB_K1_MINB, int PASSES = 1, bool GATED = false>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
   __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
@@ -154,6 +196,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashPara
     di = __shfl_sync(0xffffffffu, di, 0);
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
+    if (GATED && !warp_await_tokens(p, d, lane)) break;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -313,7 +356,7 @@ __device__ __forceinline__ uint32_t ld_shared_u8(uint32_t addr) {
 // before the epilogue.  For long documents: a launch over a few thousand full texts (a fused
 // chunk's long list) is then balanced over blocks instead of lasting as long as its slowest
 // warp (C4's fused step: 4 full texts per warp at most vs ~2.7 per warp with one each).
-template <int NPL, bool BLOCKDOC = false>
+template <int NPL, bool BLOCKDOC = false, bool GATED = false>
 __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_minhash_scr(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
   __shared__ uint8_t qb[K1_WARPS][NPL][K1S_QCAP][32];   // [slot][lane]: conflict-free byte stores
@@ -334,7 +377,13 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
     uint32_t di = 0;
     if (BLOCKDOC) {
       __syncthreads();                                   // the previous document's merge is done
-      if (threadIdx.x == 0) s_doc = atomicAdd(p.counter, 1u);
+      if (threadIdx.x == 0) {   // (the whole block takes the gate's verdict: no barrier divergence)
+        uint32_t v = atomicAdd(p.counter, 1u);
+        const uint32_t nd = p.list ? *p.list_n : p.n_docs;
+        if (GATED && v < nd && !await_tokens(p, p.offsets[(p.list ? p.list[v] : p.doc0 + v) + 1]))
+          v = 0xFFFFFFFFu;
+        s_doc = v;
+      }
       if (BLOCKDOC)
         for (uint32_t i = threadIdx.x; i < 32u * NPL; i += K1_THREADS) smin[i] = 0xFFFFFFFFu;
       __syncthreads();
@@ -345,6 +394,7 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
     }
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
+    if (GATED && !BLOCKDOC && !warp_await_tokens(p, d, lane)) break;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -530,7 +580,7 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
 //    the candidates are evaluated exactly at the end of the chunk, all lanes in step;
 //  * PASSES > 1 walks the document PASSES times with NPL permutations each (the fingerprints are
 //    recomputed, ~2 % of the work) -- 256 permutations as 2 x 4 per lane.
-template <int NPL, int PASSES, int MINB = 3>
+template <int NPL, int PASSES, int MINB = 3, bool GATED = false>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr2(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];
   __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
@@ -546,6 +596,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr2(const Minhas
     di = __shfl_sync(0xffffffffu, di, 0);
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
+    if (GATED && !warp_await_tokens(p, d, lane)) break;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -672,60 +723,115 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr2(const Minhas
 
 template <int NPL, int PASSES, int MINB = 3>
 static int launch_s2(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash_scr2<NPL, PASSES, MINB>, K1_THREADS, 0);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  static int bps_of[2] = {0, 0};   // [gated]
+  const int gi = p.landed ? 1 : 0;
+  if (!bps_of[gi]) {
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr2<NPL, PASSES, MINB, true>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr2<NPL, PASSES, MINB, false>, K1_THREADS, 0);
+    if (bps_of[gi] < 1) bps_of[gi] = 1;
   }
+  const int blocks_per_sm = bps_of[gi];
   uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  k1_minhash_scr2<NPL, PASSES, MINB><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  if (p.landed) k1_minhash_scr2<NPL, PASSES, MINB, true><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr2<NPL, PASSES, MINB, false><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
 template <int NPL, bool BLOCKDOC = false>
 static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash_scr<NPL, BLOCKDOC>, K1_THREADS, 0);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  static int bps_of[2] = {0, 0};   // [gated]
+  const int gi = p.landed ? 1 : 0;
+  if (!bps_of[gi]) {
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr<NPL, BLOCKDOC, true>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr<NPL, BLOCKDOC, false>, K1_THREADS, 0);
+    if (bps_of[gi] < 1) bps_of[gi] = 1;
   }
+  const int blocks_per_sm = bps_of[gi];
   uint64_t want = BLOCKDOC ? (uint64_t)p.n_docs : ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  k1_minhash_scr<NPL, BLOCKDOC><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  if (p.landed) k1_minhash_scr<NPL, BLOCKDOC, true><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr<NPL, BLOCKDOC, false><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
 
 template <int NPL, int UNR, int MINB = LB_K1_MINB, int PASSES = 1>
 static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k1_minhash<NPL, UNR, MINB, PASSES>, K1_THREADS, 0);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  static int bps_of[2] = {0, 0};   // [gated]
+  const int gi = p.landed ? 1 : 0;
+  if (!bps_of[gi]) {
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash<NPL, UNR, MINB, PASSES, true>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash<NPL, UNR, MINB, PASSES, false>, K1_THREADS, 0);
+    if (bps_of[gi] < 1) bps_of[gi] = 1;
   }
+  const int blocks_per_sm = bps_of[gi];
   uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  k1_minhash<NPL, UNR, MINB, PASSES><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  if (p.landed) k1_minhash<NPL, UNR, MINB, PASSES, true><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash<NPL, UNR, MINB, PASSES, false><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
-// K1p: split this launch's documents into short (S < split_s shingles) and long ones.
-__global__ void k1_partition(const MinhashParams p, uint32_t split_s) {
-  const uint32_t di = blockIdx.x * blockDim.x + threadIdx.x;
-  if (*p.err || di >= p.n_docs) return;
-  const uint32_t d = p.doc0 + di;
+// K1p: split this launch's documents into short (S < split_s shingles) and long ones, stably
+// (each list in document order: a landing-gated launch takes its documents in list order, and
+// the tokens land in document order).  K1p1 counts long documents per 1024-document block;
+// K1p2 scans the counts of the preceding blocks and places each document with warp ballots.
+constexpr int kPartBlock = 1024;
+__device__ __forceinline__ bool is_long_doc(const MinhashParams& p, uint32_t d, uint32_t split_s) {
   const uint64_t L = p.offsets[d + 1] - p.offsets[d];
   const uint64_t S = L >= p.shingle_n ? L - p.shingle_n + 1 : 1;
-  const int which = S >= split_s ? 1 : 0;
-  const uint32_t at = atomicAdd(p.part_counts + which, 1u);
-  p.part_lists[(uint64_t)which * p.n_docs + at] = d;
+  return S >= split_s;
+}
+__global__ void __launch_bounds__(kPartBlock) k1_partition_count(const MinhashParams p, uint32_t split_s) {
+  __shared__ uint32_t wsum[kPartBlock / 32];
+  if (*p.err) return;
+  const uint32_t di = blockIdx.x * kPartBlock + threadIdx.x;
+  const bool lg = di < p.n_docs && is_long_doc(p, p.doc0 + di, split_s);
+  const uint32_t bal = __ballot_sync(0xffffffffu, lg);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = wsum[threadIdx.x];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) p.part_blk[blockIdx.x] = v;
+  }
+}
+__global__ void __launch_bounds__(kPartBlock) k1_partition_place(const MinhashParams p, uint32_t split_s) {
+  __shared__ uint32_t wl[kPartBlock / 32];
+  __shared__ uint32_t base_long;
+  if (*p.err) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w == 0) {   // long documents in the preceding blocks
+    uint32_t acc = 0;
+    for (uint32_t b = lane; b < blockIdx.x; b += 32) acc += p.part_blk[b];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) base_long = acc;
+  }
+  const uint32_t di = blockIdx.x * kPartBlock + threadIdx.x;
+  const bool in = di < p.n_docs;
+  const bool lg = in && is_long_doc(p, p.doc0 + di, split_s);
+  const uint32_t bal = __ballot_sync(0xffffffffu, lg);
+  if (lane == 0) wl[w] = __popc(bal);
+  __syncthreads();
+  uint32_t before = 0;                          // long documents of the earlier warps of the block
+  for (int i = 0; i < w; i++) before += wl[i];
+  const uint32_t rank_long = base_long + before + __popc(bal & ((1u << lane) - 1));
+  if (in) {
+    if (lg) p.part_lists[(uint64_t)p.n_docs + rank_long] = p.doc0 + di;
+    else p.part_lists[di - rank_long] = p.doc0 + di;        // short rank = documents before - long before
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kPartBlock - 1) {
+    const uint32_t n_long = rank_long + (lg ? 1 : 0);
+    p.part_counts[0] = p.n_docs - n_long;
+    p.part_counts[1] = n_long;
+  }
 }
 
 int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps) {
@@ -747,16 +853,25 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
       const char* e = getenv("LSHBLOOM_K1_SPLIT_S");
       split_s = e ? (uint32_t)atoi(e) : 1024u;
     }
-    cudaMemsetAsync(p.part_counts, 0, 2 * sizeof(uint32_t), s);
-    k1_partition<<<(p.n_docs + 255) / 256, 256, 0, s>>>(p, split_s);
+    const unsigned pblocks = (p.n_docs + kPartBlock - 1) / kPartBlock;
+    k1_partition_count<<<pblocks, kPartBlock, 0, s>>>(p, split_s);
+    k1_partition_place<<<pblocks, kPartBlock, 0, s>>>(p, split_s);
     MinhashParams a = p, b = p;
     a.list = p.part_lists;
     a.list_n = p.part_counts;
     b.list = p.part_lists + p.n_docs;
     b.list_n = p.part_counts + 1;
-    cudaMemsetAsync(p.counter, 0, 4, s);
-    if (max_bps == 0) launch_t<4, LB_UNR4, 4, 2>(a, sm_count, s, 0);   // 256 = 2 passes x 4 x 32
-    else launch_t<4, LB_UNR4, LB_K1_MINB, 2>(a, sm_count, s, max_bps);
+    auto short_docs = [&] {
+      cudaMemsetAsync(p.counter, 0, 4, s);
+      if (max_bps == 0) launch_t<4, LB_UNR4, 4, 2>(a, sm_count, s, 0);   // 256 = 2 passes x 4 x 32
+      else launch_t<4, LB_UNR4, LB_K1_MINB, 2>(a, sm_count, s, max_bps);
+    };
+    // With a landing gate (host batch still being copied) the long documents go first: the short
+    // ones (~2 % of C3's) are spread over the whole batch, and their kernel would wait for the
+    // copy's end with every warp parked on one of them.
+    static const bool long_first_env = [] { const char* e = getenv("LSHBLOOM_K1_LONG_FIRST"); return e && atoi(e); }();
+    const bool long_first = p.landed || long_first_env;
+    if (!long_first) short_docs();
     // long documents: a warp each when there are enough of them to balance the warps (>= 16 per
     // resident warp), else a block each (a few thousand full texts over ~2400 warps would last as
     // long as the slowest warp: C4's fused step 43.9 -> 37.2 ms); both kernels are launched and
@@ -771,7 +886,8 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     else launch_s2<8, 1>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
-    return 4;
+    if (long_first) short_docs();
+    return 5;
   }
   const bool screened = mode == 1 || (mode == 2 && npl >= 8);
   if (screened && npl <= 8) {

@@ -348,11 +348,16 @@ print("ok")
 @pytest.mark.parametrize("env", [{"LSHBLOOM_K1_ALT": "0"},
                                  {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_FUSE_EDGE": "1024"},
                                  {"LSHBLOOM_FUSE_DOCS": "1500", "LSHBLOOM_FUSE_EDGE": "1100", "LSHBLOOM_K1_ALT": "1"},
-                                 {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_HOST_BUFS": "3", "LSHBLOOM_HOST_MIN_DOCS": "300"},
-                                 {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_HOST_BUFS": "2", "LSHBLOOM_HOST_MIN_DOCS": "300"}])
+                                 {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_HOST_BUFS": "3", "LSHBLOOM_HOST_MIN_DOCS": "300",
+                                  "LSHBLOOM_LANDING": "0"},
+                                 {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_HOST_BUFS": "2", "LSHBLOOM_HOST_MIN_DOCS": "300",
+                                  "LSHBLOOM_LANDING": "0"},
+                                 {"LSHBLOOM_FUSE_DOCS": "1024", "LSHBLOOM_LAND_LOG2": "18"},
+                                 {"LSHBLOOM_LAND_LOG2": "18", "LSHBLOOM_BLOOM_PATH": "sweep", "LSHBLOOM_FUSE_DOCS_SWEEP": "2048"}])
 def test_fused_chunking_knobs(env):
     # the fused step's K1 chunking (one or two K1 streams, chunk sizes, 2 or 3 host staging
-    # buffers, the host chunk floor) changes only the schedule:
+    # buffers, the host chunk floor, landing-gated host batches with 2^18-token pieces, with
+    # either Bloom path) changes only the schedule:
     # flags equal the oracle's with 128 and 256 permutations (the latter with the length-split
     # K1 and its per-stream partition scratch), device and host inputs, many chunks per call
     import os
