@@ -446,7 +446,8 @@ def main():
                 print("p2p exchange unavailable (%s); using NCCL" % e, file=sys.stderr)
                 sx.exchange = args.exchange = "nccl"
         eng = sx.engine
-        step = lambda o, t: sx.query_insert(o, t)  # noqa: E731
+        counts = [args.docs] * world                 # fixed per-rank batches: no count all-gather
+        step = lambda o, t: sx.query_insert(o, t, counts=counts)  # noqa: E731
     else:
         eng = LSHBloom(cfg.num_perm, cfg.b, cfg.r, args.n_expected, cfg.fp_rate, cfg.seed, device=local,
                        sub_batch=args.sub_batch, index=args.index)
@@ -542,7 +543,7 @@ def main():
         p_tok = torch.from_numpy(tok.view(np.int32)).pin_memory()
         if world > 1:
             e2e_step = lambda: sx.query_insert(p_off.to(dev, non_blocking=True),  # noqa: E731
-                                               p_tok.to(dev, non_blocking=True)).cpu()
+                                               p_tok.to(dev, non_blocking=True), counts=counts).cpu()
         else:
             h_flags = torch.empty(args.docs, dtype=torch.uint8).pin_memory()
             if args.sync_steps:

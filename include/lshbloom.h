@@ -105,6 +105,9 @@ typedef struct {
     uint32_t sweep_log2_window; /* sweep window 2^w bits, w in [10, 19] (0 = chosen per batch) */
     uint32_t sweep_cap;  /* sweep records per bin before the exact layout (0 = from the batch's
                             expected load; tests use tiny values to force the exact layout) */
+    double lsh_threshold;/* Jaccard threshold T the (b, r) were chosen for, carried
+                            into the LSHB checkpoint header; 0 = unknown: the header then holds
+                            (1/b)^(1/r), the S-curve's approximate threshold.  No effect on results */
 } lshbloom_config;
 
 /* Bloom paths.  Both evaluate the same stream-order rule -- bit g of band j is set before
@@ -168,6 +171,7 @@ typedef struct {
     uint32_t index_kind;      /* LSHBLOOM_INDEX_BLOOM / _CLASSIC / _BLOCKED */
     uint64_t classic_slots;   /* classic: table slots per band (0 for Bloom) */
     uint64_t sweeps;          /* batches (or 4M-document pieces) applied by the sweep path */
+    double lsh_threshold;     /* the configured Jaccard threshold (0 = unknown) */
 } lshbloom_info_t;
 
 /* Create an index of b Bloom filters: sizes them from (n_expected, fp_rate),
@@ -293,7 +297,8 @@ LSHBLOOM_API int lshbloom_stage_times(lshbloom *h, int32_t enable, double *ms_ou
 
 /* Checkpoint / resume.
  * lshbloom_save writes the index (world = 1 handles) as SPEC's little-endian "LSHB" container:
- *   "LSHB" | version u32 (1) | threshold f64 ((1/b)^(1/r), the S-curve midpoint; create takes b,r)
+ *   "LSHB" | version u32 (1) | threshold f64 (config lsh_threshold; if 0, (1/b)^(1/r), the S-curve
+ *            midpoint -- create takes b, r; load carries it back into the config)
  *   | num_perm u32 | b u32 | r u32 | signature_seed u64 | band_hash_seed u64 (both = seed)
  *   | n_docs u64 (n_expected) | p_effective f64 (1-(1-p)^b) | doc_count u64
  *   | b filter encodings | CRC32C u32 of every preceding byte,

@@ -39,7 +39,7 @@ class _Config(ctypes.Structure):
                 ("device", ctypes.c_int32), ("rank", ctypes.c_uint32), ("world", ctypes.c_uint32),
                 ("sub_batch", ctypes.c_uint32), ("index_kind", ctypes.c_uint32),
                 ("bloom_path", ctypes.c_uint32), ("sweep_log2_window", ctypes.c_uint32),
-                ("sweep_cap", ctypes.c_uint32)]
+                ("sweep_cap", ctypes.c_uint32), ("lsh_threshold", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -51,7 +51,7 @@ class _Info(ctypes.Structure):
                 ("oversubscribed", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("n_expected", ctypes.c_uint64), ("fp_rate", ctypes.c_double),
                 ("index_kind", ctypes.c_uint32), ("classic_slots", ctypes.c_uint64),
-                ("sweeps", ctypes.c_uint64)]
+                ("sweeps", ctypes.c_uint64), ("lsh_threshold", ctypes.c_double)]
 
 
 class _Plan(ctypes.Structure):
@@ -172,13 +172,15 @@ class LSHBloom:
     def __init__(self, num_perm: int, b: int, r: int, n_expected: int, fp_rate: float, seed: int = 0,
                  *, shingle_n: int = 5, device: int | None = None, rank: int = 0, world: int = 1,
                  sub_batch: int = 0, index: str = "bloom", bloom_path: str = "auto", sweep_window_log2: int = 0,
-                 sweep_cap: int = 0, _handle=None):
+                 sweep_cap: int = 0, lsh_threshold: float = 0.0, _handle=None):
         """index: "bloom" (the paper's per-band Bloom filters), "classic" (the exact
         band-equality MinHashLSH index it replaces; fp_rate is ignored) or "blocked" (a blocked
         Bloom variant: all k probes of a band hash in one 1024-bit block).
         bloom_path: "auto", "random" (K3-K6, random access per probe) or "sweep" (K7-K9, windows
         streamed through shared memory); results are identical.  sweep_window_log2 / sweep_cap
-        override the sweep's window size (2^w bits, w in [10, 19]) and bin capacity."""
+        override the sweep's window size (2^w bits, w in [10, 19]) and bin capacity.
+        lsh_threshold: the Jaccard threshold the (b, r) were chosen for, recorded in checkpoints
+        (0: unknown, (1/b)^(1/r) is recorded)."""
         self._lib = lib()
         kinds = {"bloom": 0, "classic": 1, "blocked": 2}
         if index not in kinds:
@@ -194,7 +196,7 @@ class LSHBloom:
                 raise ValueError("bloom_path must be 'auto', 'random' or 'sweep'")
             cfg = _Config(num_perm, b, r, shingle_n, n_expected, fp_rate, seed & (2**64 - 1), device,
                           rank, world, sub_batch, kinds[index], BLOOM_PATHS[bloom_path], sweep_window_log2,
-                          sweep_cap)
+                          sweep_cap, float(lsh_threshold))
             h = ctypes.c_void_p()
             rc = self._lib.lshbloom_create_ex(ctypes.byref(cfg), ctypes.byref(h))
             if rc:

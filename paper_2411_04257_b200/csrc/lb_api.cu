@@ -1107,6 +1107,8 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   if (c.bloom_path > LSHBLOOM_PATH_SWEEP) return fail(nullptr, LSHBLOOM_EUSAGE, "bloom_path must be 0 (auto), 1 (random) or 2 (sweep)");
   if (c.sweep_log2_window && (c.sweep_log2_window < 10 || c.sweep_log2_window > 19))
     return fail(nullptr, LSHBLOOM_EUSAGE, "sweep_log2_window must be 0 or in [10, 19]");
+  if (!(c.lsh_threshold >= 0.0 && c.lsh_threshold <= 1.0))
+    return fail(nullptr, LSHBLOOM_EUSAGE, "lsh_threshold must be 0 (unknown) or in (0, 1]");
   if (c.world == 0) c.world = 1;
   if (c.rank >= c.world) return fail(nullptr, LSHBLOOM_EUSAGE, "rank must be < world");
   if (c.world > c.b) return fail(nullptr, LSHBLOOM_EUSAGE, "world must be <= b (every rank owns >= 1 band)");
@@ -1660,6 +1662,7 @@ int lshbloom_info(const lshbloom* h, lshbloom_info_t* out) {
   out->n_expected = h->cfg.n_expected;
   out->fp_rate = h->cfg.fp_rate;
   out->index_kind = h->cfg.index_kind;
+  out->lsh_threshold = h->cfg.lsh_threshold;
   out->sweeps = h->sweeps;
   if (h->cfg.index_kind == LSHBLOOM_INDEX_CLASSIC) {
     out->classic_slots = 1ull << h->c_log2cap;
@@ -1836,7 +1839,8 @@ int lshbloom_save(lshbloom* h, const char* path) {
   if (!f) return fail(h, LSHBLOOM_EIO, std::string("cannot open ") + path + " for writing");
   Writer w{f};
   const lshbloom_config& c = h->cfg;
-  const double threshold = pow(1.0 / c.b, 1.0 / c.r);
+  // the threshold the (b, r) were chosen for; unknown: the S-curve's approximate (1/b)^(1/r)
+  const double threshold = c.lsh_threshold > 0.0 ? c.lsh_threshold : pow(1.0 / c.b, 1.0 / c.r);
   const double p_eff = -expm1((double)c.b * log1p(-c.fp_rate));
   w.put("LSHB", 4, false);
   w.put_v<uint32_t>(1, false);
@@ -1940,6 +1944,7 @@ int lshbloom_load(const char* path, int32_t device, lshbloom** out) {
       c.seed = sseed;
       c.device = device;
       c.world = 1;
+      c.lsh_threshold = threshold > 0.0 && threshold <= 1.0 ? threshold : 0.0;
       int rc = lshbloom_create_ex(&c, &h);
       if (rc) return bail(rc == LSHBLOOM_EUSAGE ? LSHBLOOM_EFORMAT : rc, "header parameters rejected: " + g_create_error, nullptr);
       created = true;

@@ -72,11 +72,17 @@ class ShardedLSHBloom:
         dist.all_gather(out, t, group=self.group)
         return [int(x.item()) for x in out]
 
-    def query_insert(self, offsets, tokens):
-        """Local documents' duplicate flags (uint8), global stream order = rank order."""
+    def query_insert(self, offsets, tokens, counts: list[int] | None = None):
+        """Local documents' duplicate flags (uint8), global stream order = rank order.
+        counts: every rank's document count of this batch, when the caller knows them (the
+        same list on every rank); otherwise they are all-gathered (one host sync per batch)."""
         device = offsets.device
         n_local = offsets.numel() - 1
-        counts = self._counts(n_local, device)
+        if counts is None:
+            counts = self._counts(n_local, device)
+        elif len(counts) != self.world or counts[self.rank] != n_local:
+            raise ValueError("counts must list every rank's document count (this rank: %d)" % n_local)
+        counts = [int(c) for c in counts]
         if self.exchange == "p2p":
             return self._query_insert_p2p(offsets, tokens, counts, device)
         if self.pipeline_docs > 0:

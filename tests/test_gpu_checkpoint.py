@@ -73,6 +73,21 @@ def test_file_layout_matches_spec_and_oracle_filters(stream, tmp_path):
         assert f["payload"] == ref.filter_bytes(j).tobytes()      # bit-exact filter state vs oracle
 
 
+def test_configured_threshold_round_trips(stream, tmp_path):
+    """The header's threshold field holds the T the (b, r) were chosen for when the config names
+    it (SPEC LshParams), and load carries it back."""
+    cfg, off, tok, bh, dup, ref = stream
+    idx = LSHBloom(128, 16, 8, 2000, 1e-3, 7, device=0, lsh_threshold=0.8)
+    assert idx.info()["lsh_threshold"] == 0.8
+    path = str(tmp_path / "t.lshb")
+    idx.save(path)
+    hdr, _ = read_lshb(open(path, "rb").read())
+    assert hdr["threshold"] == 0.8
+    assert LSHBloom.load(path, device=0).info()["lsh_threshold"] == 0.8
+    with pytest.raises(LSHBloomError):
+        LSHBloom(128, 16, 8, 2000, 1e-3, 7, device=0, lsh_threshold=1.5)
+
+
 def test_corrupt_truncated_and_foreign_files(stream, tmp_path):
     cfg, off, tok, bh, dup, ref = stream
     idx = LSHBloom(128, 16, 8, 2000, 1e-3, 7, device=0)

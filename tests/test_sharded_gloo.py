@@ -67,7 +67,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cuts, n_total, out_path, pipeline_docs=0):
+def _worker(rank, world, port, cuts, n_total, out_path, pipeline_docs=0, pass_counts=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -78,15 +78,18 @@ def _worker(rank, world, port, cuts, n_total, out_path, pipeline_docs=0):
     for batch in cuts:                       # several batches: filter state persists across calls
         a, b = batch[rank], batch[rank + 1]
         off, tok = gen_range(cfg, a, b)
-        got = sx.query_insert(torch.from_numpy(off.view(np.int64)), torch.from_numpy(tok.view(np.int32)))
+        counts = [batch[r + 1] - batch[r] for r in range(world)] if pass_counts else None
+        got = sx.query_insert(torch.from_numpy(off.view(np.int64)), torch.from_numpy(tok.view(np.int32)),
+                              counts=counts)
         flags.append(got.numpy().copy())
     np.save(out_path % rank, np.concatenate(flags))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,pipeline_docs", [(2, 0), (3, 0), (2, 97), (3, 500), (3, 1 << 18)])
-def test_sharded_flags_equal_single_process_oracle(world, pipeline_docs, tmp_path):
+@pytest.mark.parametrize("world,pipeline_docs,pass_counts", [(2, 0, False), (3, 0, False), (2, 97, False),
+                                                             (3, 500, False), (3, 1 << 18, False), (3, 500, True)])
+def test_sharded_flags_equal_single_process_oracle(world, pipeline_docs, pass_counts, tmp_path):
     # two stream batches; each split into `world` unequal contiguous rank shards
     rng = np.random.default_rng(world)
     bounds = [0, 1400, 1401, 3000]                       # includes a one-document batch
@@ -98,7 +101,8 @@ def test_sharded_flags_equal_single_process_oracle(world, pipeline_docs, tmp_pat
         inner = sorted(rng.choice(np.arange(a + 1, b), world - 1, replace=False).tolist())
         cuts.append([a] + inner + [b])
     out = str(tmp_path / "flags_%d.npy")
-    mp.spawn(_worker, args=(world, _free_port(), cuts, bounds[-1], out, pipeline_docs), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), cuts, bounds[-1], out, pipeline_docs, pass_counts), nprocs=world,
+             join=True)
     got = []
     per_rank = [np.load(out % r) for r in range(world)]
     # reassemble global order: batch by batch, rank by rank
