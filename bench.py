@@ -160,12 +160,14 @@ def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 102
     return total, total, 0
 
 
-# K1 issue bounds per evaluation on the fmaheavy pipe (IMAD.WIDE.U32 0.25 warp-instr/clk/SMSP,
-# 32-bit IMAD 0.5; tools/micro/pipe_micro.cu, profiles/pipe_micro.txt): the exact form needs four
-# 32x32->64 products (16 pipe cycles per warp-evaluation -> 2 evaluations/clk/SMSP); the screened
-# form (long documents) decides almost every evaluation from two IMAD.WIDE + two 32-bit IMAD
-# (12 cycles -> 8/3 evaluations/clk/SMSP).
-K1_EVALS_PER_CLK_SMSP = {"exact": 2.0, "screened": 8.0 / 3.0}
+# K1 bounds per evaluation (tools/micro/pipe_micro.cu, profiles/r02h_microbench.txt +
+# r02j_pipe.txt: IMAD.WIDE.U32 and DFMA 0.25 warp-instr/clk/SMSP on one shared unit, 32-bit IMAD
+# 0.5 on fmaheavy, overlapping DFMA): the exact form needs four 32x32->64 products (16 cycles per
+# warp-evaluation -> 2 evaluations/clk/SMSP); the screened form (long documents, 256
+# permutations, lb_minhash.cu k1_minhash_scr3) decides almost every evaluation from two DFMA + two
+# 32-bit IMAD (8 cycles of the DFMA unit -> 4 evaluations/clk/SMSP; its issue count, 8.2
+# instructions per evaluation in the SASS, is the same bound to within 3 %).
+K1_EVALS_PER_CLK_SMSP = {"exact": 2.0, "screened": 4.0}
 
 
 def k1_peak(evals, f_hz: float, sms: int = 148):
@@ -579,8 +581,9 @@ def main():
                 "kernel": "k1_minhash (fingerprints + MinHash + band hashes)",
                 "peak_source": "%s sm_max_mhz %.0f x 148 SMs x 4 SMSP x evaluations/clk/SMSP of the kernel each "
                                "document runs on (exact: 2 = four IMAD.WIDE at 1/4 rate; screened, >= 1024 "
-                               "shingles with 256 permutations: 8/3 = two IMAD.WIDE + two IMAD), weighted by "
-                               "evaluations" % (peak_src, f_max / 1e6),
+                               "shingles with 256 permutations: 4 = two DFMA at 1/4 rate beside two IMAD), "
+                               "weighted by evaluations" % (peak_src, f_max / 1e6),
+                "frac_of_exact_form_bound": (achieved / (2.0 * 148 * 4 * f_max)) if achieved else None,
                 "evals_per_launch": evals[0], "evals_exact_kernel": evals[1], "evals_screened_kernel": evals[2],
                 "ms_per_launch": k1_per_launch_ms,
                 "share_of_step": (k1_ms / max(1, args.steps)) / (ms / args.steps)}

@@ -740,6 +740,205 @@ static int launch_s2(const MinhashParams& p, int sm_count, cudaStream_t s, int m
   return 1;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Screened K1 with the FP64 pipe (k1_minhash_scr3).  The integer screen needs the high half of
+// the 64-bit products (two IMAD.WIDE: 8 of its 12 fmaheavy cycles per warp-evaluation).  Split
+// instead a = ah 2^32 + al, x = xh 2^32 + xl (ah, xh < 2^29) and M = ah xl + al xh (< 2^62):
+//   a x = al xl + M 2^32 + ah xh 2^64,   M 2^32 = M_hi 2^61 + M_lo 2^32  (M_hi = floor(M / 2^29)),
+//   2^61 = 1, 2^64 = 8 (mod P)  =>  a x + b = T (mod P),  T = al xl + M_lo 2^32 + M_hi + 8 ah xh + b,
+//   0 <= T < 2^64 + 3 2^61 + 2^33 < 11 2^61 + 2^33, so q = floor(T / P) <= 11 and
+//   y = low32((a x + b) mod P) = L + q (mod 2^32),  L = lo(al xl) + lo(8ah xh) + M_hi + lo(b).
+// M_hi is only needed to within +-1 for a screen, and two DFMA give that:
+//   r = fma(ah, xl 2^-29, fma(al, xh 2^-29, 1.5 2^52))  (every operand exact in binary64; both
+//   results lie in [2^52, 2^53) where the ulp is 1, so each rounding moves by <= 1/2) = 1.5 2^52
+//   + M / 2^29 + eps, |eps| <= 1, and the low word of r is N mod 2^32 with N - M_hi in {-1, 0, 1}.
+// With L' = lo(al xl) + lo(8ah xh) + N + lo(b) = L + e, e in [-1, 1]: L in [m, 2^32 - 1 - 11]
+// guarantees y >= m, and L' in [m + 1, 2^32 - 13] guarantees that, i.e.
+//   w = L' - (m + 1)  <=  K = 2^32 - 14 - m   (mod 2^32)  =>  skip;  otherwise a candidate,
+// evaluated exactly (eval_exact).  DFMA issues at 1/4 rate on the unit IMAD.WIDE uses, IMAD at 1/2
+// on fmaheavy, and the two overlap (tools/micro/pipe_micro.cu: fma.f64 + mad.lo 0.494 warp-inst/clk
+// /SMSP together), so a screen costs 8 cycles of the FP64 unit instead of 12 of fmaheavy; the
+// whole screen loop runs at 2.36 evaluations/clk/SMSP in isolation vs 1.91 for the integer one
+// (tools/micro/dfma_screen.cu, which also checks 2^32 random and near-P triples: no screened-out
+// y < m).  B200 (GB100) has full-rate-for-Blackwell FP64; on parts with vestigial FP64 this
+// kernel must not be selected.
+constexpr uint32_t kScr3Q = 13;   // K = 2^32 - 1 - kScr3Q - m: q <= 11 plus the +-1 of N
+struct __align__(16) XLimbsF {     // shingle x for the FP64 screen
+  double XL, XH;                   // xl 2^-29, xh 2^-29 (exact)
+  uint32_t xl, xh;                 // x mod 2^32, x >> 32
+};
+__device__ __forceinline__ uint32_t screen_w_f64(uint32_t al, uint32_t a8h, double AL, double AH, const XLimbsF& x,
+                                                 uint32_t bias) {
+  const double r1 = fma(AL, x.XH, 6755399441055744.0);   // 1.5 2^52
+  const double r2 = fma(AH, x.XL, r1);
+  return al * x.xl + a8h * x.xh + (uint32_t)__double2loint(r2) + bias;
+}
+
+template <int NPL, int PASSES, int MINB = 3, bool GATED = false>
+__global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const MinhashParams p) {
+  __shared__ XLimbs xs[K1_WARPS][32];        // exact-evaluation limbs
+  __shared__ XLimbsF xf[K1_WARPS][32];       // screen limbs
+  __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (*p.err) return;
+  if (p.block_gate && p.list && *p.list_n < p.block_gate) return;   // the block-per-document kernel runs
+  const uint64_t tpol = l2_evict_first_policy();
+
+  for (;;) {
+    uint32_t di = 0;
+    if (lane == 0) di = atomicAdd(p.counter, 1u);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (di >= (p.list ? *p.list_n : p.n_docs)) break;
+    const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
+    if (GATED && !warp_await_tokens(p, d, lane)) break;
+    const uint64_t o0 = p.offsets[d];
+    const uint64_t L = p.offsets[d + 1] - o0;
+    LB_ASSERT(L >= 1 && o0 >= p.tok_base);
+    const uint32_t* tk = p.tokens + (o0 - p.tok_base);
+    const uint32_t n = p.shingle_n;
+    const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;
+    const uint32_t t = L >= n ? n : (uint32_t)L;
+    const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
+
+    for (int pass = 0; pass < PASSES; pass++) {
+      const uint32_t pm0 = pass * 32 * NPL + lane;           // permutation of slot q: pm0 + 32 q
+      uint32_t al[NPL], a8h[NPL], bias[NPL], K[NPL];
+      double AL[NPL], AH[NPL];
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const PermCoef c = p.coef[pm0 + 32 * q];             // a = a1 2^31 + a0
+        al[q] = c.a0 | (c.a1 << 31);
+        a8h[q] = (c.a1 >> 1) << 3;
+        AL[q] = (double)al[q];
+        AH[q] = (double)(c.a1 >> 1);
+      }
+      bool exact_mode = false;
+      for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        if (s < S) {
+          uint64_t h = init;
+          for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
+          const uint64_t x = mod_p(h);
+          xs[w][lane] = make_limbs(h);
+          XLimbsF f;
+          f.xl = (uint32_t)x;
+          f.xh = (uint32_t)(x >> 32);
+          f.XL = (double)f.xl * 0x1p-29;
+          f.XH = (double)f.xh * 0x1p-29;
+          xf[w][lane] = f;
+        }
+        __syncwarp();
+        const uint32_t cnt = min(32u, S - s0);
+        uint32_t j = 0;
+        if (s0 == 0) {   // seed the minima with the first shingle, exactly
+          const XLimbs x0 = xs[w][0];
+          bool big = false;
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);     // (the raw minimum, for now)
+            big |= K[q] > 0xFFFFFFFFu - kScr3Q;
+          }
+          exact_mode = __any_sync(0xffffffffu, big);
+          if (!exact_mode) {
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+              bias[q] = p.coef[pm0 + 32 * q].b0 - K[q] - 1u;
+              K[q] = 0xFFFFFFFFu - kScr3Q - K[q];
+            }
+          }
+          j = 1;
+        }
+        if (exact_mode) {     // (probability ~2^-28 per document) K holds the raw minima
+          for (; j < cnt; j++) {
+            const XLimbs xv = xs[w][j];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(p.coef[pm0 + 32 * q], xv));
+          }
+        } else {
+          uint32_t mask[NPL];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) mask[q] = 0;
+          for (; j + 4 <= cnt; j += 4) {
+            XLimbsF xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) xv[u] = xf[w][j + u];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+#pragma unroll
+              for (int u = 0; u < 4; u++)
+                if (screen_w_f64(al[q], a8h[q], AL[q], AH[q], xv[u], bias[q]) > K[q]) mask[q] |= 1u << (j + u);
+            }
+          }
+          for (; j < cnt; j++) {
+            const XLimbsF xv = xf[w][j];
+#pragma unroll
+            for (int q = 0; q < NPL; q++)
+              if (screen_w_f64(al[q], a8h[q], AL[q], AH[q], xv, bias[q]) > K[q]) mask[q] |= 1u << j;
+          }
+          // exact evaluation of the candidates, all lanes in step (rounds = the warp's largest count)
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            const uint32_t rounds = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(mask[q]));
+            if (!rounds) continue;
+            const PermCoef c = p.coef[pm0 + 32 * q];
+            for (uint32_t i = 0; i < rounds; i++) {
+              if (mask[q]) {
+                const uint32_t js = __ffs(mask[q]) - 1;
+                mask[q] &= mask[q] - 1;
+                const uint32_t y = eval_exact(c, xs[w][js]);
+                if (y < 0xFFFFFFFFu - kScr3Q - K[q]) {
+                  bias[q] = c.b0 - y - 1u;
+                  K[q] = 0xFFFFFFFFu - kScr3Q - y;
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const uint32_t m = exact_mode ? K[q] : 0xFFFFFFFFu - kScr3Q - K[q];
+        const uint32_t pm = pm0 + 32 * q;
+        if (p.sig_out && pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = m;
+        if (p.bh_out) sg[w][pm] = m;
+      }
+    }  // pass
+    if (p.bh_out) {
+      __syncwarp();
+      for (uint32_t jb = lane; jb < p.b; jb += 32) {
+        if (p.map.ncol[jb] == 0) continue;
+        uint64_t acc = 0;                               // BH_j, P:207-208 (DESIGN R6/R7)
+        for (uint32_t u = 0; u < p.r; u++) {
+          acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][jb * p.r + u], __ldg(p.bcoef + p.r + u));
+          acc = acc >= kP ? acc - kP : acc;
+        }
+        p.map.ptr[jb][(uint64_t)d * p.map.ncol[jb]] = acc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int NPL, int PASSES, int MINB = 3>
+static int launch_s3(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
+  static int bps_of[2] = {0, 0};   // [gated]
+  const int gi = p.landed ? 1 : 0;
+  if (!bps_of[gi]) {
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr3<NPL, PASSES, MINB, true>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr3<NPL, PASSES, MINB, false>, K1_THREADS, 0);
+    if (bps_of[gi] < 1) bps_of[gi] = 1;
+  }
+  const int blocks_per_sm = bps_of[gi];
+  uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
+  const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
+  uint64_t grid = (uint64_t)sm_count * bps;
+  if (want < grid) grid = want ? want : 1;
+  if (p.landed) k1_minhash_scr3<NPL, PASSES, MINB, true><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr3<NPL, PASSES, MINB, false><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  return 1;
+}
+
 template <int NPL, bool BLOCKDOC = false>
 static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int bps_of[2] = {0, 0};   // [gated]
@@ -878,12 +1077,15 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     // the one the device-side count does not select returns at once
     b.block_gate = 16u * (uint32_t)sm_count * 2u * K1_WARPS;
     cudaMemsetAsync(p.counter, 0, 4, s);
-    // warp-per-document long documents: the lean screened kernel (80 registers, 3 blocks per SM;
-    // C3 200K full texts alone: 102.0 ms vs 111.4 ms for k1_minhash_scr; 2 x 4 permutations per
-    // lane at 4 blocks: 108.2 ms; LSHBLOOM_K1_SCR=1 selects the older kernel)
-    static const int scr = [] { const char* e = getenv("LSHBLOOM_K1_SCR"); return e ? atoi(e) : 2; }();
+    // warp-per-document long documents: the FP64-screen kernel, 8 permutations per lane in one
+    // pass (128 registers, 2 blocks per SM; C3 200K full texts alone: 82.6 ms; 2 x 4 per lane at 3
+    // blocks: 90.4 ms; the integer screens: 101.8 ms k1_minhash_scr2 = LSHBLOOM_K1_SCR=2, 111.4 ms
+    // k1_minhash_scr = 1)
+    static const int scr = [] { const char* e = getenv("LSHBLOOM_K1_SCR"); return e ? atoi(e) : 4; }();
     if (scr == 1) launch_s<8, false>(b, sm_count, s, max_bps);
-    else launch_s2<8, 1>(b, sm_count, s, max_bps);
+    else if (scr == 2) launch_s2<8, 1>(b, sm_count, s, max_bps);
+    else if (scr == 3) launch_s3<4, 2>(b, sm_count, s, max_bps);
+    else launch_s3<8, 1, 2>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
     if (long_first) short_docs();

@@ -26,6 +26,12 @@ __global__ void k(uint32_t seed, uint32_t* out, unsigned long long* cyc) {
       if (OP == 8) asm volatile("mad.lo.u32 %0, %0, %1, %2;\n\tlop3.b32 %1, %1, %0, %2, 0x96;" : "+r"(x), "+r"(y) : "r"(z));
       if (OP == 9) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(x) : "r"(y), "r"(z));
       if (OP == 10) asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %2;" : "+r"(x), "+r"(y) : "r"(z));
+      // FP64 (the screen's high half, tools/micro/dfma_screen.cu): operands as u32 pairs
+      if (OP == 11) asm volatile("{.reg .f64 d, e; mov.b64 d, {%0, %1}; mov.b64 e, {%2, %2}; fma.rn.f64 d, d, e, d; mov.b64 {%0, %1}, d;}" : "+r"(x), "+r"(y) : "r"(z));
+      if (OP == 12) asm volatile("{.reg .f64 d, e; mov.b64 d, {%0, %1}; mov.b64 e, {%2, %2}; fma.rn.f64 d, d, e, d; mov.b64 {%0, %1}, d;}\n\t"
+                                 "mad.lo.u32 %2, %2, %0, %1;" : "+r"(x), "+r"(y), "+r"(z));
+      if (OP == 13) asm volatile("{.reg .f64 d, e; mov.b64 d, {%0, %1}; mov.b64 e, {%2, %2}; fma.rn.f64 d, d, e, d; mov.b64 {%0, %1}, d;}\n\t"
+                                 "{.reg .u64 t; mul.wide.u32 t, %2, %2; mov.b64 {%2, %1}, t;}" : "+r"(x), "+r"(y), "+r"(z));
     }
   }
   unsigned long long t1 = clock64();
@@ -51,5 +57,6 @@ int main() {
   run<0>("mul.wide.u32", 1); run<1>("mul.hi.u32", 1); run<2>("mad.lo.u32", 1); run<3>("add.u32 x2 (1 IADD3)", 1);
   run<4>("lop3", 1); run<5>("shf", 1); run<6>("min+max", 2); run<7>("mad.wide+add64 (~3)", 3);
   run<8>("mad.lo + lop3", 2); run<9>("mad.hi.u32", 1); run<10>("add.cc+addc", 2);
+  run<11>("fma.rn.f64", 1); run<12>("fma.f64 + mad.lo", 2); run<13>("fma.f64 + mul.wide", 2);
   return 0;
 }
