@@ -753,25 +753,27 @@ static int launch_s2(const MinhashParams& p, int sm_count, cudaStream_t s, int m
 //   results lie in [2^52, 2^53) where the ulp is 1, so each rounding moves by <= 1/2) = 1.5 2^52
 //   + M / 2^29 + eps, |eps| <= 1, and the low word of r is N mod 2^32 with N - M_hi in {-1, 0, 1}.
 // With L' = lo(al xl) + lo(8ah xh) + N + lo(b) = L + e, e in [-1, 1]: L in [m, 2^32 - 1 - 11]
-// guarantees y >= m, and L' in [m + 1, 2^32 - 13] guarantees that, i.e.
-//   w = L' - (m + 1)  <=  K = 2^32 - 14 - m   (mod 2^32)  =>  skip;  otherwise a candidate,
-// evaluated exactly (eval_exact).  DFMA issues at 1/4 rate on the unit IMAD.WIDE uses, IMAD at 1/2
+// guarantees y >= m, and L' in [m + 1, 2^32 - 13] guarantees that, i.e. with u = L' + 12 and
+// T = m + 13 (mod 2^32):  u >= T  =>  skip;  u < T: a candidate, evaluated exactly (eval_exact).
+// (m > 2^32 - 14, only possible for a document's first shingle, keeps the document exact.)  The
+// constant lo(b) + 12 rides in the magic addend: r1 = fma(al, xh 2^-29, 1.5 2^52 + lo(b) + 12)
+// (exact: < 2^53), so u = al xl + 8ah xh + lo32(r2) -- two IMAD, no add.  DFMA issues at 1/4 rate on the unit IMAD.WIDE uses, IMAD at 1/2
 // on fmaheavy, and the two overlap (tools/micro/pipe_micro.cu: fma.f64 + mad.lo 0.494 warp-inst/clk
 // /SMSP together), so a screen costs 8 cycles of the FP64 unit instead of 12 of fmaheavy; the
 // whole screen loop runs at 2.36 evaluations/clk/SMSP in isolation vs 1.91 for the integer one
 // (tools/micro/dfma_screen.cu, which also checks 2^32 random and near-P triples: no screened-out
 // y < m).  B200 (GB100) has full-rate-for-Blackwell FP64; on parts with vestigial FP64 this
 // kernel must not be selected.
-constexpr uint32_t kScr3Q = 13;   // K = 2^32 - 1 - kScr3Q - m: q <= 11 plus the +-1 of N
+constexpr uint32_t kScr3Q = 13;   // T = m + kScr3Q: q <= 11 plus the +-1 of N, plus 1
 struct __align__(16) XLimbsF {     // shingle x for the FP64 screen
   double XL, XH;                   // xl 2^-29, xh 2^-29 (exact)
   uint32_t xl, xh;                 // x mod 2^32, x >> 32
 };
-__device__ __forceinline__ uint32_t screen_w_f64(uint32_t al, uint32_t a8h, double AL, double AH, const XLimbsF& x,
-                                                 uint32_t bias) {
-  const double r1 = fma(AL, x.XH, 6755399441055744.0);   // 1.5 2^52
+__device__ __forceinline__ uint32_t screen_u_f64(uint32_t al, uint32_t a8h, double AL, double AH, double CB,
+                                                 const XLimbsF& x) {
+  const double r1 = fma(AL, x.XH, CB);                   // CB = 1.5 2^52 + lo(b) + 12
   const double r2 = fma(AH, x.XL, r1);
-  return al * x.xl + a8h * x.xh + (uint32_t)__double2loint(r2) + bias;
+  return al * x.xl + a8h * x.xh + (uint32_t)__double2loint(r2);
 }
 
 template <int NPL, int PASSES, int MINB = 3, bool GATED = false>
@@ -802,8 +804,8 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
 
     for (int pass = 0; pass < PASSES; pass++) {
       const uint32_t pm0 = pass * 32 * NPL + lane;           // permutation of slot q: pm0 + 32 q
-      uint32_t al[NPL], a8h[NPL], bias[NPL], K[NPL];
-      double AL[NPL], AH[NPL];
+      uint32_t al[NPL], a8h[NPL], K[NPL];                   // K: the threshold T = m + 13 (raw m in exact mode)
+      double AL[NPL], AH[NPL], CB[NPL];
 #pragma unroll
       for (int q = 0; q < NPL; q++) {
         const PermCoef c = p.coef[pm0 + 32 * q];             // a = a1 2^31 + a0
@@ -811,6 +813,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
         a8h[q] = (c.a1 >> 1) << 3;
         AL[q] = (double)al[q];
         AH[q] = (double)(c.a1 >> 1);
+        CB[q] = 6755399441055744.0 + (double)(c.b0 + 12u);   // 1.5 2^52 + lo(b) + 12 (mod 2^32)
       }
       bool exact_mode = false;
       for (uint32_t s0 = 0; s0 < S; s0 += 32) {
@@ -836,15 +839,12 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
 #pragma unroll
           for (int q = 0; q < NPL; q++) {
             K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);     // (the raw minimum, for now)
-            big |= K[q] > 0xFFFFFFFFu - kScr3Q;
+            big |= K[q] > 0xFFFFFFFFu - kScr3Q;               // T = m + 13 would wrap
           }
           exact_mode = __any_sync(0xffffffffu, big);
           if (!exact_mode) {
 #pragma unroll
-            for (int q = 0; q < NPL; q++) {
-              bias[q] = p.coef[pm0 + 32 * q].b0 - K[q] - 1u;
-              K[q] = 0xFFFFFFFFu - kScr3Q - K[q];
-            }
+            for (int q = 0; q < NPL; q++) K[q] += kScr3Q;
           }
           j = 1;
         }
@@ -866,14 +866,14 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
             for (int q = 0; q < NPL; q++) {
 #pragma unroll
               for (int u = 0; u < 4; u++)
-                if (screen_w_f64(al[q], a8h[q], AL[q], AH[q], xv[u], bias[q]) > K[q]) mask[q] |= 1u << (j + u);
+                if (screen_u_f64(al[q], a8h[q], AL[q], AH[q], CB[q], xv[u]) < K[q]) mask[q] |= 1u << (j + u);
             }
           }
           for (; j < cnt; j++) {
             const XLimbsF xv = xf[w][j];
 #pragma unroll
             for (int q = 0; q < NPL; q++)
-              if (screen_w_f64(al[q], a8h[q], AL[q], AH[q], xv, bias[q]) > K[q]) mask[q] |= 1u << j;
+              if (screen_u_f64(al[q], a8h[q], AL[q], AH[q], CB[q], xv) < K[q]) mask[q] |= 1u << j;
           }
           // exact evaluation of the candidates, all lanes in step (rounds = the warp's largest count)
 #pragma unroll
@@ -886,10 +886,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
                 const uint32_t js = __ffs(mask[q]) - 1;
                 mask[q] &= mask[q] - 1;
                 const uint32_t y = eval_exact(c, xs[w][js]);
-                if (y < 0xFFFFFFFFu - kScr3Q - K[q]) {
-                  bias[q] = c.b0 - y - 1u;
-                  K[q] = 0xFFFFFFFFu - kScr3Q - y;
-                }
+                if (y < K[q] - kScr3Q) K[q] = y + kScr3Q;    // (y < m; y + 13 may wrap for a false candidate)
               }
             }
           }
@@ -898,7 +895,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
       }
 #pragma unroll
       for (int q = 0; q < NPL; q++) {
-        const uint32_t m = exact_mode ? K[q] : 0xFFFFFFFFu - kScr3Q - K[q];
+        const uint32_t m = exact_mode ? K[q] : K[q] - kScr3Q;
         const uint32_t pm = pm0 + 32 * q;
         if (p.sig_out && pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = m;
         if (p.bh_out) sg[w][pm] = m;
@@ -1078,9 +1075,10 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     b.block_gate = 16u * (uint32_t)sm_count * 2u * K1_WARPS;
     cudaMemsetAsync(p.counter, 0, 4, s);
     // warp-per-document long documents: the FP64-screen kernel, 8 permutations per lane in one
-    // pass (128 registers, 2 blocks per SM; C3 200K full texts alone: 82.6 ms; 2 x 4 per lane at 3
-    // blocks: 90.4 ms; the integer screens: 101.8 ms k1_minhash_scr2 = LSHBLOOM_K1_SCR=2, 111.4 ms
-    // k1_minhash_scr = 1)
+    // pass (128 registers, 2 blocks per SM; C3 200K full texts alone: 81.2 ms; 2 x 4 per lane at 3
+    // blocks, LSHBLOOM_K1_SCR=3: 90.4 ms; the integer screens: 101.8 ms k1_minhash_scr2 = 2,
+    // 111.4 ms k1_minhash_scr = 1; a min over each 4-shingle group with the mask bits built in a
+    // branch: 86.1 ms; the same min with the flagged groups re-screened after the chunk: 109.8 ms)
     static const int scr = [] { const char* e = getenv("LSHBLOOM_K1_SCR"); return e ? atoi(e) : 4; }();
     if (scr == 1) launch_s<8, false>(b, sm_count, s, max_bps);
     else if (scr == 2) launch_s2<8, 1>(b, sm_count, s, max_bps);
