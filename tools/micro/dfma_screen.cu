@@ -41,7 +41,7 @@ __device__ __forceinline__ uint32_t wval(const Slot& s, const XS& x, uint32_t bi
 
 __global__ void check(uint64_t seed, uint64_t n, unsigned long long* stats) {
   uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  unsigned long long fn = 0, cand = 0, below = 0;
+  unsigned long long fn = 0, cand = 0, below = 0, fn_shipped = 0, cand_shipped = 0;
   for (; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r0 = mix(seed + 3 * i), r1 = mix(seed + 3 * i + 1), r2 = mix(seed + 3 * i + 2);
     uint64_t a = 1 + r0 % (kP - 1), x = r1 % kP, b = (r2 >> 3) % kP;
@@ -59,10 +59,19 @@ __global__ void check(uint64_t seed, uint64_t n, unsigned long long* stats) {
     cand += is_cand;
     below += y < m;
     fn += (y < m) && !is_cand;
+    // the shipped form (lb_minhash.cu k1_minhash_scr3): lo(b) + 12 in the magic addend, u < m + 13
+    const double CB = kMagic + (double)((uint32_t)b + 12u);
+    const double q1 = fma(s.AL, xs.XH, CB), q2 = fma(s.AH, xs.XL, q1);
+    const uint32_t u = s.al * xs.xl + s.a8h * xs.xh + (uint32_t)__double2loint(q2);
+    const bool cand2 = m <= 0xFFFFFFFFu - 13u ? u < m + 13u : true;
+    cand_shipped += cand2;
+    fn_shipped += (y < m) && !cand2;
   }
   atomicAdd(stats + 0, fn);
   atomicAdd(stats + 1, cand);
   atomicAdd(stats + 2, below);
+  atomicAdd(stats + 3, fn_shipped);
+  atomicAdd(stats + 4, cand_shipped);
 }
 
 // ---- rates
@@ -141,14 +150,15 @@ void run_rate(const char* name, const uint32_t* dC, uint32_t* dO, unsigned long 
 
 int main() {
   unsigned long long* st;
-  cudaMalloc(&st, 24);
-  cudaMemset(st, 0, 24);
+  cudaMalloc(&st, 40);
+  cudaMemset(st, 0, 40);
   const uint64_t n = 1ull << 32;
   check<<<148 * 8, 256>>>(12345, n, st);
-  unsigned long long h[3];
-  cudaMemcpy(h, st, 24, cudaMemcpyDeviceToHost);
-  printf("{\"check_triples\": %llu, \"false_negatives\": %llu, \"candidates\": %llu, \"y_below_m\": %llu, \"err\": \"%s\"}\n",
-         (unsigned long long)n, h[0], h[1], h[2], cudaGetErrorString(cudaGetLastError()));
+  unsigned long long h[5];
+  cudaMemcpy(h, st, 40, cudaMemcpyDeviceToHost);
+  printf("{\"check_triples\": %llu, \"false_negatives\": %llu, \"candidates\": %llu, \"y_below_m\": %llu, "
+         "\"false_negatives_shipped_form\": %llu, \"candidates_shipped_form\": %llu, \"err\": \"%s\"}\n",
+         (unsigned long long)n, h[0], h[1], h[2], h[3], h[4], cudaGetErrorString(cudaGetLastError()));
   uint32_t hC[1024];
   uint64_t s = 7;
   for (int i = 0; i < 1024; i++) { s = s * 6364136223846793005ull + 1442695040888963407ull; hC[i] = (uint32_t)(s >> 32); }
