@@ -919,6 +919,7 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
   int rc;
   if (sp.use && (rc = sweep_alloc(h, sp, h->bloom_stream))) return rc;
   const BloomParams bp = bloom_params(h, bh, n, 1, ddup, nullptr);
+  p.beside_random_bloom = sp.use ? 0u : 1u;
   // K1 chunks alternate between the K1 streams: each launch ends with a tail in which its last
   // documents finish on a few warps, and the next chunk's blocks fill the SM slots meanwhile.
   // Each stream has its own work counter, partition scratch and staging buffer (host batches).

@@ -81,6 +81,8 @@ struct MinhashParams {
   uint32_t* part_counts;     // [2]
   uint32_t* part_blk;        // [ceil(n_docs / 1024)]: long documents per partition block
   uint32_t block_gate;       // screened kernel: block-per-document mode iff *list_n < block_gate
+  uint32_t exact_prefix;     // FP64-screen kernel: 32-shingle chunks evaluated exactly before screening
+  uint32_t beside_random_bloom;  // K1 runs beside the random-access Bloom kernels (kernel choice only)
   // Landing gate (host batches streamed into one device token buffer while K1 runs): the copy
   // engine lands the tokens in pieces of 2^land_log2 tokens, in order, and after piece i a
   // stream memory operation (no SM involved) writes *landed = i + 1.  A warp starts document d

@@ -815,7 +815,12 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
         AH[q] = (double)(c.a1 >> 1);
         CB[q] = 6755399441055744.0 + (double)(c.b0 + 12u);   // 1.5 2^52 + lo(b) + 12 (mod 2^32)
       }
-      bool exact_mode = false;
+      // exact prefix: the first p.exact_prefix chunks are evaluated exactly (K = raw minima), where
+      // candidates would be frequent (P(candidate) ~ 1/s after s shingles); then the screen
+      bool exact_mode = true;
+#pragma unroll
+      for (int q = 0; q < NPL; q++) K[q] = 0xFFFFFFFFu;
+      const uint32_t pre = 32u * p.exact_prefix;
       for (uint32_t s0 = 0; s0 < S; s0 += 32) {
         const uint32_t s = s0 + lane;
         if (s < S) {
@@ -833,22 +838,22 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
         __syncwarp();
         const uint32_t cnt = min(32u, S - s0);
         uint32_t j = 0;
-        if (s0 == 0) {   // seed the minima with the first shingle, exactly
-          const XLimbs x0 = xs[w][0];
+        if (exact_mode && s0 >= pre) {   // leave exact mode (seeding with shingle 0 if no prefix)
           bool big = false;
+          const XLimbs x0 = xs[w][0];
 #pragma unroll
           for (int q = 0; q < NPL; q++) {
-            K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);     // (the raw minimum, for now)
+            if (s0 == 0) K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);   // (the raw minimum, for now)
             big |= K[q] > 0xFFFFFFFFu - kScr3Q;               // T = m + 13 would wrap
           }
+          if (s0 == 0) j = 1;
           exact_mode = __any_sync(0xffffffffu, big);
           if (!exact_mode) {
 #pragma unroll
             for (int q = 0; q < NPL; q++) K[q] += kScr3Q;
           }
-          j = 1;
         }
-        if (exact_mode) {     // (probability ~2^-28 per document) K holds the raw minima
+        if (exact_mode) {     // the prefix, or (probability ~2^-28) a minimum near 2^32: raw minima
           for (; j < cnt; j++) {
             const XLimbs xv = xs[w][j];
 #pragma unroll
@@ -1038,7 +1043,20 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
   static int mode = -1;
   if (mode < 0) {
     const char* e = getenv("LSHBLOOM_K1");
-    mode = !e ? 2 : (e[0] == 'e' ? 0 : 1);
+    mode = !e ? 2 : (e[0] == 'e' ? 0 : (e[0] == 'h' ? 3 : 1));
+  }
+  // 65-128 permutations (C1, C2, C5): the FP64-screen kernel with the documents' first 32
+  // shingles evaluated exactly (where candidates are dense) unless the caller runs K1 beside the
+  // random-access Bloom kernels (L2-resident filters), whose latency-bound kernels need the SM room
+  // the 92-register exact kernel leaves (C2 step 18.9 vs 19.4 ms with the screen at 2 blocks per
+  // SM).  K1 alone on C2 batches: 14.1 vs 17.1 ms; C5 fused sweep step 46.6 vs 53.3 ms per 2M
+  // documents (prefix 0 / 1 / 2 / 3 / 4 chunks: 18.0 / 14.1 / 14.8 / 15.7 / 16.8 ms on C2).
+  // LSHBLOOM_K1=exact keeps the exact kernel everywhere, =hyb forces the screen.
+  if (npl == 4 && (mode == 3 || (mode == 2 && !p.beside_random_bloom))) {
+    static const uint32_t pre = [] { const char* e = getenv("LSHBLOOM_K1_PREFIX"); return e ? (uint32_t)atoi(e) : 1u; }();
+    MinhashParams q = p;
+    q.exact_prefix = pre;
+    return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
   }
   if (mode == 2 && npl == 8 && p.part_lists && p.n_docs > 0) {
     // 256 permutations: the screened kernel wins on full-text lengths (C3: 1760 vs 1236 Geval/s)

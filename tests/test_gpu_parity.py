@@ -287,8 +287,11 @@ def test_many_chunks_short_docs(on_device):
     assert (u64(idx.band_hashes(*args)) == bh).all()
 
 
-@pytest.mark.parametrize("mode", ["exact", "screened"])
+@pytest.mark.parametrize("mode", ["exact", "screened", "hyb:0", "hyb:1", "hyb:3", "scr:2", "scr:3"])
 def test_both_minhash_kernels(mode):
+    # exact / screened: LSHBLOOM_K1 for every launch; hyb:k the FP64-screen kernel with a k-chunk
+    # exact prefix for 128 permutations; scr:k the long-document kernel of the 256-permutation
+    # split (2: integer screen, 3: FP64 screen in two passes; default: FP64 screen, one pass)
     # run in a subprocess: the kernel choice is read once per process from LSHBLOOM_K1
     import os
     import subprocess
@@ -309,7 +312,15 @@ for name, n in (("C1", 3000), ("C3", 300)):
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, LSHBLOOM_K1=mode, PYTHONPATH=root)
+    env = dict(os.environ, PYTHONPATH=root)
+    kind, _, arg = mode.partition(":")
+    if kind == "hyb":
+        env.update(LSHBLOOM_K1="hyb", LSHBLOOM_K1_PREFIX=arg)
+    elif kind == "scr":
+        env.update(LSHBLOOM_K1_SCR=arg)
+        env.pop("LSHBLOOM_K1", None)
+    else:
+        env.update(LSHBLOOM_K1=mode)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
