@@ -941,6 +941,232 @@ static int launch_s3(const MinhashParams& p, int sm_count, cudaStream_t s, int m
   return 1;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Screened K1 with the FP32 pipe (k1_minhash_scr4; round 2).  Same split and T as scr3:
+//   y = low32((a x + b) mod P) = L + H + q (mod 2^32),  L = lo(al xl) + lo(8ah xh) + lo(b),
+//   H = floor(M / 2^29), M = ah xl + al xh,  q in [0, 11].
+// A screen needs H only to within a few thousand, and two binary32 FMA give that:
+//   r = fmaf(AH, XL, fmaf(AL, XH, 1.5 2^34)),  AL = fl(al), AH = fl(ah), XL = fl(xl) 2^-29,
+//   XH = fl(xh) 2^-29 (each rounded to nearest: relative error <= 2^-24).  Both sums lie in
+//   [2^34, 2^35] where the ulp is 2^11, and bits(r) << 11 = r - 1.5 2^34 (mod 2^32) (at r = 2^35
+//   both sides are 2^33 = 0).  Error of Hc = bits(r) << 11 against H: the two products' operand
+//   rounding <= 2^32 (2^-23 + 2^-48) each (~2^9), the two roundings <= 2^10 each, the floor < 1:
+//   |Hc - H| <= 3074.  With u = lo(al xl) + lo(8ah xh) + (lo(b) + 4096) + Hc:
+//   u - y = 4096 + (Hc - H) - q in [1011, 7170] (mod 2^32), so for m <= 2^32 - 1 - 8192,
+//   y < m  =>  u < m + 7171 < m + 8192 = K;  u >= K: skip;  u < K: a candidate, evaluated exactly.
+// Per evaluation: 2 IMAD + 2 FFMA (one with an immediate) + a shift-add (LEA) + half a 3-input min
+// (the min over each 4-shingle group is compared once) -- the FFMA share the fma pipe with IMAD
+// but the second product's high half no longer costs a 1/4-rate DFMA or IMAD.WIDE.  Measured
+// in isolation (tools/micro/fp32_screen.cu, profiles/r02s_fp32_screen_micro.txt): 3.75
+// evaluations/clk/SMSP at 2 blocks per SM vs 2.39-2.53 for the FP64 screen; 2^32 random and
+// adversarial triples: no screened-out y < m, largest |Hc - H| 2471.
+constexpr uint32_t kScr4W = 8192, kScr4D = 4096;
+constexpr float kScr4Magic = 25769803776.0f;   // 1.5 2^34
+struct __align__(16) XLimbsS {                 // shingle x for the FP32 screen
+  uint32_t xl, xh;                             // x mod 2^32, x >> 32
+  float XL, XH;                                // fl(xl) 2^-29, fl(xh) 2^-29
+};
+__device__ __forceinline__ uint32_t screen_u_f32(uint32_t al, uint32_t a8h, uint32_t lb, float AL, float AH,
+                                                 const XLimbsS& x) {
+  const float r1 = __fmaf_rn(AL, x.XH, kScr4Magic);
+  const float r2 = __fmaf_rn(AH, x.XL, r1);
+  uint32_t t, hb;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(al), "r"(x.xl), "r"(lb));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a8h), "r"(x.xh), "r"(t));
+  asm("shl.b32 %0, %1, 11;" : "=r"(hb) : "r"(__float_as_uint(r2)));
+  return t + hb;
+}
+
+template <int NPL, int PASSES, int MINB = 2, bool GATED = false>
+__global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const MinhashParams p) {
+  __shared__ XLimbs xs[K1_WARPS][32];        // exact-evaluation limbs
+  __shared__ XLimbsS xf[K1_WARPS][32];       // screen limbs
+  __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
+  __shared__ uint32_t kq[K1_WARPS][NPL][32];  // thresholds while flagged groups are resolved
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (*p.err) return;
+  if (p.block_gate && p.list && *p.list_n < p.block_gate) return;   // the block-per-document kernel runs
+  const uint64_t tpol = l2_evict_first_policy();
+
+  for (;;) {
+    uint32_t di = 0;
+    if (lane == 0) di = atomicAdd(p.counter, 1u);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (di >= (p.list ? *p.list_n : p.n_docs)) break;
+    const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
+    if (GATED && !warp_await_tokens(p, d, lane)) break;
+    const uint64_t o0 = p.offsets[d];
+    const uint64_t L = p.offsets[d + 1] - o0;
+    LB_ASSERT(L >= 1 && o0 >= p.tok_base);
+    const uint32_t* tk = p.tokens + (o0 - p.tok_base);
+    const uint32_t n = p.shingle_n;
+    const uint32_t S = L >= n ? (uint32_t)(L - n + 1) : 1u;
+    const uint32_t t = L >= n ? n : (uint32_t)L;
+    const uint64_t init = (t == n) ? p.fp_init_n : mix64(kFpSalt + t);
+
+    for (int pass = 0; pass < PASSES; pass++) {
+      const uint32_t pm0 = pass * 32 * NPL + lane;           // permutation of slot q: pm0 + 32 q
+      uint32_t al[NPL], a8h[NPL], lb[NPL], K[NPL];          // K: the threshold m + W (raw m in exact mode)
+      float AL[NPL], AH[NPL];
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const PermCoef c = p.coef[pm0 + 32 * q];             // a = a1 2^31 + a0
+        al[q] = c.a0 | (c.a1 << 31);
+        a8h[q] = (c.a1 >> 1) << 3;
+        lb[q] = c.b0 + kScr4D;
+        AL[q] = __uint2float_rn(al[q]);
+        AH[q] = __uint2float_rn(c.a1 >> 1);
+      }
+      bool exact_mode = true;
+#pragma unroll
+      for (int q = 0; q < NPL; q++) K[q] = 0xFFFFFFFFu;
+      const uint32_t pre = 32u * p.exact_prefix;
+      for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+        const uint32_t s = s0 + lane;
+        if (s < S) {
+          uint64_t h = init;
+          for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
+          const uint64_t x = mod_p(h);
+          xs[w][lane] = make_limbs(h);
+          XLimbsS f;
+          f.xl = (uint32_t)x;
+          f.xh = (uint32_t)(x >> 32);
+          f.XL = __uint2float_rn(f.xl) * 0x1p-29f;
+          f.XH = __uint2float_rn(f.xh) * 0x1p-29f;
+          xf[w][lane] = f;
+        }
+        __syncwarp();
+        const uint32_t cnt = min(32u, S - s0);
+        uint32_t j = 0;
+        if (exact_mode && s0 >= pre) {   // leave exact mode (seeding with shingle 0 if no prefix)
+          bool big = false;
+          const XLimbs x0 = xs[w][0];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) {
+            if (s0 == 0) K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);   // (the raw minimum, for now)
+            big |= K[q] > 0xFFFFFFFFu - kScr4W;               // m + W would wrap
+          }
+          if (s0 == 0) j = 1;
+          exact_mode = __any_sync(0xffffffffu, big);
+          if (!exact_mode) {
+#pragma unroll
+            for (int q = 0; q < NPL; q++) K[q] += kScr4W;
+          }
+        }
+        if (exact_mode) {     // the prefix, or (probability ~2^-19 per permutation) a minimum near 2^32
+          for (; j < cnt; j++) {
+            const XLimbs xv = xs[w][j];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(p.coef[pm0 + 32 * q], xv));
+          }
+        } else {
+          // groups of 4 shingles from j0: bit g of mask[q] = some u of group g is below K[q]
+          const uint32_t j0 = j;
+          uint32_t mask[NPL];
+#pragma unroll
+          for (int q = 0; q < NPL; q++) mask[q] = 0;
+          uint32_t g = 0;
+          for (; j + 4 <= cnt; j += 4, g++) {
+            XLimbsS xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) xv[u] = xf[w][j + u];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+              uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+              for (int u = 0; u < 4; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u]));
+              if (mn < K[q]) mask[q] |= 1u << g;
+            }
+          }
+          // the chunk's last (cnt - j0) mod 4 shingles: exactly (warp-uniform)
+          for (; j < cnt; j++) {
+            const XLimbs xv = xs[w][j];
+#pragma unroll
+            for (int q = 0; q < NPL; q++) {
+              const uint32_t y = eval_exact(p.coef[pm0 + 32 * q], xv);
+              if (y < K[q] - kScr4W) K[q] = y + kScr4W;
+            }
+          }
+          // exact evaluation of the flagged groups: each lane walks its own (permutation, group)
+          // pairs, whichever permutation they belong to, so a round serves every lane that still
+          // has one (rounds = the warp's largest per-lane count, not a sum over permutations); the
+          // slot's coefficients come from the (L1-resident) table, its threshold from shared memory
+          uint64_t cm = 0;
+#pragma unroll
+          for (int q = 0; q < NPL; q++) cm |= (uint64_t)mask[q] << (8 * q);
+          if (__any_sync(0xffffffffu, cm != 0)) {
+#pragma unroll
+            for (int q = 0; q < NPL; q++) kq[w][q][lane] = K[q];
+            while (cm) {
+              const uint32_t bit = __ffsll(cm) - 1;
+              cm &= cm - 1;
+              const uint32_t q = bit >> 3, gs = j0 + 4 * (bit & 7);
+              const PermCoef c = p.coef[pm0 + 32 * q];
+              const uint32_t cal = c.a0 | (c.a1 << 31), ca8h = (c.a1 >> 1) << 3, clb = c.b0 + kScr4D;
+              const float cAL = __uint2float_rn(cal), cAH = __uint2float_rn(c.a1 >> 1);
+              uint32_t Kq = kq[w][q][lane];
+              // re-screen the group against the current threshold, then the passing shingles exactly
+              uint32_t pass = 0;
+#pragma unroll
+              for (uint32_t u = 0; u < 4; u++)
+                pass |= (uint32_t)(screen_u_f32(cal, ca8h, clb, cAL, cAH, xf[w][gs + u]) < Kq) << u;
+              while (pass) {
+                const uint32_t u = __ffs(pass) - 1;
+                pass &= pass - 1;
+                const uint32_t y = eval_exact(c, xs[w][gs + u]);
+                if (y < Kq - kScr4W) Kq = y + kScr4W;   // (y < m <= 2^32 - 1 - W: no wrap)
+              }
+              kq[w][q][lane] = Kq;
+            }
+#pragma unroll
+            for (int q = 0; q < NPL; q++) K[q] = kq[w][q][lane];
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int q = 0; q < NPL; q++) {
+        const uint32_t m = exact_mode ? K[q] : K[q] - kScr4W;
+        const uint32_t pm = pm0 + 32 * q;
+        if (p.sig_out && pm < p.num_perm) p.sig_out[(uint64_t)d * p.num_perm + pm] = m;
+        if (p.bh_out) sg[w][pm] = m;
+      }
+    }  // pass
+    if (p.bh_out) {
+      __syncwarp();
+      for (uint32_t jb = lane; jb < p.b; jb += 32) {
+        if (p.map.ncol[jb] == 0) continue;
+        uint64_t acc = 0;                               // BH_j, P:207-208 (DESIGN R6/R7)
+        for (uint32_t u = 0; u < p.r; u++) {
+          acc += affine32_mod_p(__ldg(p.bcoef + u), sg[w][jb * p.r + u], __ldg(p.bcoef + p.r + u));
+          acc = acc >= kP ? acc - kP : acc;
+        }
+        p.map.ptr[jb][(uint64_t)d * p.map.ncol[jb]] = acc;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int NPL, int PASSES, int MINB = 2>
+static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
+  static int bps_of[2] = {0, 0};   // [gated]
+  const int gi = p.landed ? 1 : 0;
+  if (!bps_of[gi]) {
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false>, K1_THREADS, 0);
+    if (bps_of[gi] < 1) bps_of[gi] = 1;
+  }
+  const int blocks_per_sm = bps_of[gi];
+  uint64_t want = ((uint64_t)p.n_docs + K1_WARPS - 1) / K1_WARPS;
+  const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
+  uint64_t grid = (uint64_t)sm_count * bps;
+  if (want < grid) grid = want ? want : 1;
+  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr4<NPL, PASSES, MINB, false><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  return 1;
+}
+
 template <int NPL, bool BLOCKDOC = false>
 static int launch_s(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int bps_of[2] = {0, 0};   // [gated]
@@ -1035,6 +1261,13 @@ __global__ void __launch_bounds__(kPartBlock) k1_partition_place(const MinhashPa
   }
 }
 
+// The screened kernel for long documents (LSHBLOOM_K1_SCR): 5 = the FP32 screen (default), 4 = the
+// FP64 screen, 3 = the FP64 screen at 2 x 4 permutations per lane, 2 / 1 = the integer screens.
+static int k1_scr_choice() {
+  static const int scr = [] { const char* e = getenv("LSHBLOOM_K1_SCR"); return e ? atoi(e) : 5; }();
+  return scr;
+}
+
 int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s, int max_bps) {
   // Kernel choice (measured on B200, tools/k1_variants.py): with 128 permutations (npl 4) the
   // exact kernel wins on abstract-length documents (C2: 1203 vs ~1100 Geval/s); with 256
@@ -1056,7 +1289,8 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     static const uint32_t pre = [] { const char* e = getenv("LSHBLOOM_K1_PREFIX"); return e ? (uint32_t)atoi(e) : 1u; }();
     MinhashParams q = p;
     q.exact_prefix = pre;
-    return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
+    if (k1_scr_choice() == 4) return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
+    return launch_s4<4, 1, 3>(q, sm_count, s, max_bps);
   }
   if (mode == 2 && npl == 8 && p.part_lists && p.n_docs > 0) {
     // 256 permutations: the screened kernel wins on full-text lengths (C3: 1760 vs 1236 Geval/s)
@@ -1097,11 +1331,14 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     // blocks, LSHBLOOM_K1_SCR=3: 90.4 ms; the integer screens: 101.8 ms k1_minhash_scr2 = 2,
     // 111.4 ms k1_minhash_scr = 1; a min over each 4-shingle group with the mask bits built in a
     // branch: 86.1 ms; the same min with the flagged groups re-screened after the chunk: 109.8 ms)
-    static const int scr = [] { const char* e = getenv("LSHBLOOM_K1_SCR"); return e ? atoi(e) : 4; }();
+    const int scr = k1_scr_choice();
+    static const uint32_t lpre = [] { const char* e = getenv("LSHBLOOM_K1_LPREFIX"); return e ? (uint32_t)atoi(e) : 1u; }();
+    if (scr == 5) b.exact_prefix = lpre;
     if (scr == 1) launch_s<8, false>(b, sm_count, s, max_bps);
     else if (scr == 2) launch_s2<8, 1>(b, sm_count, s, max_bps);
     else if (scr == 3) launch_s3<4, 2>(b, sm_count, s, max_bps);
-    else launch_s3<8, 1, 2>(b, sm_count, s, max_bps);
+    else if (scr == 4) launch_s3<8, 1, 2>(b, sm_count, s, max_bps);
+    else launch_s4<8, 1, 2>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
     if (long_first) short_docs();

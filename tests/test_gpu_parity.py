@@ -287,11 +287,12 @@ def test_many_chunks_short_docs(on_device):
     assert (u64(idx.band_hashes(*args)) == bh).all()
 
 
-@pytest.mark.parametrize("mode", ["exact", "screened", "hyb:0", "hyb:1", "hyb:3", "scr:2", "scr:3"])
+@pytest.mark.parametrize("mode", ["exact", "screened", "hyb:0", "hyb:1", "hyb:3", "scr:2", "scr:3", "scr:4", "scr:4+hyb:1"])
 def test_both_minhash_kernels(mode):
     # exact / screened: LSHBLOOM_K1 for every launch; hyb:k the FP64-screen kernel with a k-chunk
     # exact prefix for 128 permutations; scr:k the long-document kernel of the 256-permutation
-    # split (2: integer screen, 3: FP64 screen in two passes; default: FP64 screen, one pass)
+    # split (2: integer screen, 3: FP64 screen in two passes, 4: FP64 screen in one pass; default:
+    # the FP32 screen, which the 128-permutation hyb batches run too unless scr:4+hyb)
     # run in a subprocess: the kernel choice is read once per process from LSHBLOOM_K1
     import os
     import subprocess
@@ -313,8 +314,13 @@ print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, PYTHONPATH=root)
+    if "+" in mode:   # the FP64 screen for both the long documents and 128-permutation batches
+        env.update(LSHBLOOM_K1_SCR="4", LSHBLOOM_K1="hyb", LSHBLOOM_K1_PREFIX="1")
+        mode = "none"
     kind, _, arg = mode.partition(":")
-    if kind == "hyb":
+    if kind == "none":
+        pass
+    elif kind == "hyb":
         env.update(LSHBLOOM_K1="hyb", LSHBLOOM_K1_PREFIX=arg)
     elif kind == "scr":
         env.update(LSHBLOOM_K1_SCR=arg)
