@@ -161,13 +161,14 @@ def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 102
 
 
 # K1 bounds per evaluation (tools/micro/pipe_micro.cu, profiles/r02h_microbench.txt +
-# r02j_pipe.txt: IMAD.WIDE.U32 and DFMA 0.25 warp-instr/clk/SMSP on one shared unit, 32-bit IMAD
-# 0.5 on fmaheavy, overlapping DFMA): the exact form needs four 32x32->64 products (16 cycles per
-# warp-evaluation -> 2 evaluations/clk/SMSP); the screened form (long documents, 256
-# permutations, lb_minhash.cu k1_minhash_scr3) decides almost every evaluation from two DFMA + two
-# 32-bit IMAD (8 cycles of the DFMA unit -> 4 evaluations/clk/SMSP; its issue count, 8.2
-# instructions per evaluation in the SASS, is the same bound to within 3 %).
-K1_EVALS_PER_CLK_SMSP = {"exact": 2.0, "screened": 4.0}
+# r02j_pipe_micro_fp64.txt + r02s_fp32_screen_micro.txt): the exact form needs four 32x32->64
+# products (IMAD.WIDE.U32 at 0.25 warp-instr/clk/SMSP: 16 cycles per warp-evaluation -> 2
+# evaluations/clk/SMSP); the screened form (long documents, 256 permutations, lb_minhash.cu
+# k1_minhash_scr4) decides almost every evaluation from two 32-bit IMAD and two FFMA, all on the
+# fma pipe: IMAD 2 cycles each, the FFMA with an immediate 1, the other 2 -> 7 cycles per
+# warp-evaluation = 32/7 = 4.57 evaluations/clk/SMSP (measured for that instruction pair alone:
+# 4.555).  (The round-2 FP64 screen, k1_minhash_scr3, was bounded at 4 by its two DFMA.)
+K1_EVALS_PER_CLK_SMSP = {"exact": 2.0, "screened": 32.0 / 7.0}
 
 
 def k1_peak(evals, f_hz: float, sms: int = 148):
@@ -581,7 +582,8 @@ def main():
                 "kernel": "k1_minhash (fingerprints + MinHash + band hashes)",
                 "peak_source": "%s sm_max_mhz %.0f x 148 SMs x 4 SMSP x evaluations/clk/SMSP of the kernel each "
                                "document runs on (exact: 2 = four IMAD.WIDE at 1/4 rate; screened, >= 1024 "
-                               "shingles with 256 permutations: 4 = two DFMA at 1/4 rate beside two IMAD), "
+                               "shingles with 256 permutations: 32/7 = two IMAD + two FFMA on the fma pipe, 7 cycles per "
+                               "warp-evaluation), "
                                "weighted by evaluations" % (peak_src, f_max / 1e6),
                 "frac_of_exact_form_bound": (achieved / (2.0 * 148 * 4 * f_max)) if achieved else None,
                 "evals_per_launch": evals[0], "evals_exact_kernel": evals[1], "evals_screened_kernel": evals[2],

@@ -1021,11 +1021,36 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
 #pragma unroll
       for (int q = 0; q < NPL; q++) K[q] = 0xFFFFFFFFu;
       const uint32_t pre = 32u * p.exact_prefix;
+      // Tokens (shingles of <= 8 ids): one coalesced 32-token load per chunk, issued a chunk ahead
+      // (tw0 = tokens [s0, s0 + 32), tw1 = [s0 + 32, s0 + 64), tw2 in flight), and the shingle's
+      // ids gathered with shuffles -- the per-lane chain of t dependent loads held the warps at the
+      // start of every chunk (ncu: 17 % of the stall samples for 5 % of the instructions).
+      const bool shfl_fp = t <= 8;
+      uint32_t tw0 = 0, tw1 = 0;
+      if (shfl_fp) {
+        if (lane < L) tw0 = ld_token(tk + lane, tpol);
+        if (32 + lane < L) tw1 = ld_token(tk + 32 + lane, tpol);
+      }
       for (uint32_t s0 = 0; s0 < S; s0 += 32) {
         const uint32_t s = s0 + lane;
-        if (s < S) {
-          uint64_t h = init;
+        uint32_t tw2 = 0;
+        if (shfl_fp && s0 + 64 + lane < L) tw2 = ld_token(tk + s0 + 64 + lane, tpol);
+        uint64_t h = init;
+        if (shfl_fp) {
+#pragma unroll
+          for (uint32_t j = 0; j < 8; j++) {
+            if (j < t) {
+              const uint32_t src = (lane + j) & 31;
+              const uint32_t a0 = __shfl_sync(0xffffffffu, tw0, src), a1 = __shfl_sync(0xffffffffu, tw1, src);
+              h = mix64(h ^ (uint64_t)(lane + j < 32 ? a0 : a1));
+            }
+          }
+          tw0 = tw1;
+          tw1 = tw2;
+        } else if (s < S) {
           for (uint32_t j = 0; j < t; j++) h = mix64(h ^ (uint64_t)ld_token(tk + s + j, tpol));
+        }
+        if (s < S) {
           const uint64_t x = mod_p(h);
           xs[w][lane] = make_limbs(h);
           XLimbsS f;
@@ -1333,11 +1358,12 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     // branch: 86.1 ms; the same min with the flagged groups re-screened after the chunk: 109.8 ms)
     const int scr = k1_scr_choice();
     static const uint32_t lpre = [] { const char* e = getenv("LSHBLOOM_K1_LPREFIX"); return e ? (uint32_t)atoi(e) : 1u; }();
-    if (scr == 5) b.exact_prefix = lpre;
+    if (scr >= 5) b.exact_prefix = lpre;
     if (scr == 1) launch_s<8, false>(b, sm_count, s, max_bps);
     else if (scr == 2) launch_s2<8, 1>(b, sm_count, s, max_bps);
     else if (scr == 3) launch_s3<4, 2>(b, sm_count, s, max_bps);
     else if (scr == 4) launch_s3<8, 1, 2>(b, sm_count, s, max_bps);
+    else if (scr == 6) launch_s4<8, 1, 3>(b, sm_count, s, max_bps);   // (3 blocks per SM: diagnostic)
     else launch_s4<8, 1, 2>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
