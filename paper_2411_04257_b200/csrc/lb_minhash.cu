@@ -1315,6 +1315,7 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     MinhashParams q = p;
     q.exact_prefix = pre;
     if (k1_scr_choice() == 4) return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
+    if (k1_scr_choice() == 7) return launch_s4<4, 1, 2>(q, sm_count, s, max_bps);
     return launch_s4<4, 1, 3>(q, sm_count, s, max_bps);
   }
   if (mode == 2 && npl == 8 && p.part_lists && p.n_docs > 0) {
