@@ -977,7 +977,7 @@ __device__ __forceinline__ uint32_t screen_u_f32(uint32_t al, uint32_t a8h, uint
   return t + hb;
 }
 
-template <int NPL, int PASSES, int MINB = 2, bool GATED = false>
+template <int NPL, int PASSES, int MINB = 2, bool GATED = false, int G = 4>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const MinhashParams p) {
   __shared__ XLimbs xs[K1_WARPS][32];        // exact-evaluation limbs
   __shared__ XLimbsS xf[K1_WARPS][32];       // screen limbs
@@ -1091,19 +1091,19 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
 #pragma unroll
           for (int q = 0; q < NPL; q++) mask[q] = 0;
           uint32_t g = 0;
-          for (; j + 4 <= cnt; j += 4, g++) {
-            XLimbsS xv[4];
+          for (; j + G <= cnt; j += G, g++) {
+            XLimbsS xv[G];
 #pragma unroll
-            for (int u = 0; u < 4; u++) xv[u] = xf[w][j + u];
+            for (int u = 0; u < G; u++) xv[u] = xf[w][j + u];
 #pragma unroll
             for (int q = 0; q < NPL; q++) {
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
-              for (int u = 0; u < 4; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u]));
+              for (int u = 0; u < G; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u]));
               if (mn < K[q]) mask[q] |= 1u << g;
             }
           }
-          // the chunk's last (cnt - j0) mod 4 shingles: exactly (warp-uniform)
+          // the chunk's last (cnt - j0) mod G shingles: exactly (warp-uniform)
           for (; j < cnt; j++) {
             const XLimbs xv = xs[w][j];
 #pragma unroll
@@ -1125,7 +1125,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
             while (cm) {
               const uint32_t bit = __ffsll(cm) - 1;
               cm &= cm - 1;
-              const uint32_t q = bit >> 3, gs = j0 + 4 * (bit & 7);
+              const uint32_t q = bit >> 3, gs = j0 + G * (bit & 7);
               const PermCoef c = p.coef[pm0 + 32 * q];
               const uint32_t cal = c.a0 | (c.a1 << 31), ca8h = (c.a1 >> 1) << 3, clb = c.b0 + kScr4D;
               const float cAL = __uint2float_rn(cal), cAH = __uint2float_rn(c.a1 >> 1);
@@ -1133,7 +1133,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
               // re-screen the group against the current threshold, then the passing shingles exactly
               uint32_t pass = 0;
 #pragma unroll
-              for (uint32_t u = 0; u < 4; u++)
+              for (uint32_t u = 0; u < G; u++)
                 pass |= (uint32_t)(screen_u_f32(cal, ca8h, clb, cAL, cAH, xf[w][gs + u]) < Kq) << u;
               while (pass) {
                 const uint32_t u = __ffs(pass) - 1;
@@ -1173,13 +1173,13 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
   }
 }
 
-template <int NPL, int PASSES, int MINB = 2>
+template <int NPL, int PASSES, int MINB = 2, int G = 4>
 static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int bps_of[2] = {0, 0};   // [gated]
   const int gi = p.landed ? 1 : 0;
   if (!bps_of[gi]) {
-    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true>, K1_THREADS, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false>, K1_THREADS, 0);
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true, G>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false, G>, K1_THREADS, 0);
     if (bps_of[gi] < 1) bps_of[gi] = 1;
   }
   const int blocks_per_sm = bps_of[gi];
@@ -1187,8 +1187,8 @@ static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int m
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
-  else k1_minhash_scr4<NPL, PASSES, MINB, false><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true, G><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr4<NPL, PASSES, MINB, false, G><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
@@ -1316,6 +1316,7 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     q.exact_prefix = pre;
     if (k1_scr_choice() == 4) return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
     if (k1_scr_choice() == 7) return launch_s4<4, 1, 2>(q, sm_count, s, max_bps);
+    if (k1_scr_choice() == 9) return launch_s4<4, 1, 3, 8>(q, sm_count, s, max_bps);
     return launch_s4<4, 1, 3>(q, sm_count, s, max_bps);
   }
   if (mode == 2 && npl == 8 && p.part_lists && p.n_docs > 0) {
@@ -1365,7 +1366,8 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     else if (scr == 3) launch_s3<4, 2>(b, sm_count, s, max_bps);
     else if (scr == 4) launch_s3<8, 1, 2>(b, sm_count, s, max_bps);
     else if (scr == 6) launch_s4<8, 1, 3>(b, sm_count, s, max_bps);   // (3 blocks per SM: diagnostic)
-    else launch_s4<8, 1, 2>(b, sm_count, s, max_bps);
+    else if (scr == 8) launch_s4<8, 1, 2, 4>(b, sm_count, s, max_bps);   // (4-shingle groups: diagnostic)
+    else launch_s4<8, 1, 2, 8>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
     if (long_first) short_docs();
