@@ -977,10 +977,11 @@ __device__ __forceinline__ uint32_t screen_u_f32(uint32_t al, uint32_t a8h, uint
   return t + hb;
 }
 
-template <int NPL, int PASSES, int MINB = 2, bool GATED = false, int G = 4>
+template <int NPL, int PASSES, int MINB = 2, bool GATED = false, int G = 4, int R = 1>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const MinhashParams p) {
-  __shared__ XLimbs xs[K1_WARPS][32];        // exact-evaluation limbs
-  __shared__ XLimbsS xf[K1_WARPS][32];       // screen limbs
+  static_assert(R == 1 || (R == 2 && G == 8), "deferred resolution packs two chunks' 4 groups");
+  __shared__ XLimbs xs[R][K1_WARPS][32];     // exact-evaluation limbs (R chunks)
+  __shared__ XLimbsS xf[R][K1_WARPS][32];    // screen limbs
   __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
   __shared__ uint32_t kq[K1_WARPS][NPL][32];  // thresholds while flagged groups are resolved
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1031,11 +1032,17 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
         if (lane < L) tw0 = ld_token(tk + lane, tpol);
         if (32 + lane < L) tw1 = ld_token(tk + 32 + lane, tpol);
       }
-      for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+      uint64_t cm = 0;                  // flagged (permutation, group) bits of the unresolved chunks
+      uint32_t j0s0 = 0, j0s1 = 0;      // first screened shingle of the chunks in buffers 0 / 1
+      for (uint32_t s0 = 0, ci = 0; s0 < S; s0 += 32, ci++) {
         const uint32_t s = s0 + lane;
+        const uint32_t bf = R == 2 ? (ci & 1) : 0;   // limb buffer of this chunk
         uint32_t tw2 = 0;
         if (shfl_fp && s0 + 64 + lane < L) tw2 = ld_token(tk + s0 + 64 + lane, tpol);
         uint64_t h = init;
+#ifdef LB_DIAG_NOFP
+        if (s0 >= 64) { tw0 = tw1; tw1 = tw2; h = (uint64_t)(s + 1) * 0x9E3779B97F4A7C15ull + o0; } else   // diagnostic: cheap distinct x
+#endif
         if (shfl_fp) {
 #pragma unroll
           for (uint32_t j = 0; j < 8; j++) {
@@ -1052,20 +1059,20 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
         }
         if (s < S) {
           const uint64_t x = mod_p(h);
-          xs[w][lane] = make_limbs(h);
+          xs[bf][w][lane] = make_limbs(h);
           XLimbsS f;
           f.xl = (uint32_t)x;
           f.xh = (uint32_t)(x >> 32);
           f.XL = __uint2float_rn(f.xl) * 0x1p-29f;
           f.XH = __uint2float_rn(f.xh) * 0x1p-29f;
-          xf[w][lane] = f;
+          xf[bf][w][lane] = f;
         }
         __syncwarp();
         const uint32_t cnt = min(32u, S - s0);
         uint32_t j = 0;
         if (exact_mode && s0 >= pre) {   // leave exact mode (seeding with shingle 0 if no prefix)
           bool big = false;
-          const XLimbs x0 = xs[w][0];
+          const XLimbs x0 = xs[bf][w][0];
 #pragma unroll
           for (int q = 0; q < NPL; q++) {
             if (s0 == 0) K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);   // (the raw minimum, for now)
@@ -1080,13 +1087,13 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
         }
         if (exact_mode) {     // the prefix, or (probability ~2^-19 per permutation) a minimum near 2^32
           for (; j < cnt; j++) {
-            const XLimbs xv = xs[w][j];
+            const XLimbs xv = xs[bf][w][j];
 #pragma unroll
             for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(p.coef[pm0 + 32 * q], xv));
           }
         } else {
           // groups of 4 shingles from j0: bit g of mask[q] = some u of group g is below K[q]
-          const uint32_t j0 = j;
+          if (bf) j0s1 = j; else j0s0 = j;
           uint32_t mask[NPL];
 #pragma unroll
           for (int q = 0; q < NPL; q++) mask[q] = 0;
@@ -1094,7 +1101,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
           for (; j + G <= cnt; j += G, g++) {
             XLimbsS xv[G];
 #pragma unroll
-            for (int u = 0; u < G; u++) xv[u] = xf[w][j + u];
+            for (int u = 0; u < G; u++) xv[u] = xf[bf][w][j + u];
 #pragma unroll
             for (int q = 0; q < NPL; q++) {
               uint32_t mn = 0xFFFFFFFFu;
@@ -1105,47 +1112,53 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
           }
           // the chunk's last (cnt - j0) mod G shingles: exactly (warp-uniform)
           for (; j < cnt; j++) {
-            const XLimbs xv = xs[w][j];
+            const XLimbs xv = xs[bf][w][j];
 #pragma unroll
             for (int q = 0; q < NPL; q++) {
               const uint32_t y = eval_exact(p.coef[pm0 + 32 * q], xv);
               if (y < K[q] - kScr4W) K[q] = y + kScr4W;
             }
           }
-          // exact evaluation of the flagged groups: each lane walks its own (permutation, group)
-          // pairs, whichever permutation they belong to, so a round serves every lane that still
-          // has one (rounds = the warp's largest per-lane count, not a sum over permutations); the
-          // slot's coefficients come from the (L1-resident) table, its threshold from shared memory
-          uint64_t cm = 0;
 #pragma unroll
-          for (int q = 0; q < NPL; q++) cm |= (uint64_t)mask[q] << (8 * q);
-          if (__any_sync(0xffffffffu, cm != 0)) {
+          for (int q = 0; q < NPL; q++) cm |= (uint64_t)mask[q] << (8 * q + (R == 2 ? 4 * bf : 0));
+        }
+        // exact evaluation of the flagged groups (every chunk, or with R = 2 every second chunk and
+        // the last: a chunk's flags wait in cm while the next chunk is screened against the older
+        // threshold, and one set of rounds serves both): each lane walks its own (permutation,
+        // group) pairs, whichever permutation they belong to, so a round serves every lane that
+        // still has one (rounds = the warp's largest per-lane count, not a sum over permutations);
+        // the slot's coefficients come from the (L1-resident) table, its threshold from shared memory
+#ifdef LB_DIAG_NORES
+        K[0] ^= (uint32_t)__popcll(cm) & 1u;   // diagnostic build only: skip the resolution (wrong signatures)
+        cm = 0;
+#endif
+        if ((R == 1 || bf == 1 || s0 + 32 >= S) && __any_sync(0xffffffffu, cm != 0)) {
 #pragma unroll
-            for (int q = 0; q < NPL; q++) kq[w][q][lane] = K[q];
-            while (cm) {
-              const uint32_t bit = __ffsll(cm) - 1;
-              cm &= cm - 1;
-              const uint32_t q = bit >> 3, gs = j0 + G * (bit & 7);
-              const PermCoef c = p.coef[pm0 + 32 * q];
-              const uint32_t cal = c.a0 | (c.a1 << 31), ca8h = (c.a1 >> 1) << 3, clb = c.b0 + kScr4D;
-              const float cAL = __uint2float_rn(cal), cAH = __uint2float_rn(c.a1 >> 1);
-              uint32_t Kq = kq[w][q][lane];
-              // re-screen the group against the current threshold, then the passing shingles exactly
-              uint32_t pass = 0;
+          for (int q = 0; q < NPL; q++) kq[w][q][lane] = K[q];
+          while (cm) {
+            const uint32_t bit = __ffsll(cm) - 1;
+            cm &= cm - 1;
+            const uint32_t hb = R == 2 ? ((bit >> 2) & 1) : 0;          // the chunk's buffer
+            const uint32_t q = bit >> 3, gs = (hb ? j0s1 : j0s0) + G * (R == 2 ? (bit & 3) : (bit & 7));
+            const PermCoef c = p.coef[pm0 + 32 * q];
+            const uint32_t cal = c.a0 | (c.a1 << 31), ca8h = (c.a1 >> 1) << 3, clb = c.b0 + kScr4D;
+            const float cAL = __uint2float_rn(cal), cAH = __uint2float_rn(c.a1 >> 1);
+            uint32_t Kq = kq[w][q][lane];
+            // re-screen the group against the current threshold, then the passing shingles exactly
+            uint32_t pass = 0;
 #pragma unroll
-              for (uint32_t u = 0; u < G; u++)
-                pass |= (uint32_t)(screen_u_f32(cal, ca8h, clb, cAL, cAH, xf[w][gs + u]) < Kq) << u;
-              while (pass) {
-                const uint32_t u = __ffs(pass) - 1;
-                pass &= pass - 1;
-                const uint32_t y = eval_exact(c, xs[w][gs + u]);
-                if (y < Kq - kScr4W) Kq = y + kScr4W;   // (y < m <= 2^32 - 1 - W: no wrap)
-              }
-              kq[w][q][lane] = Kq;
+            for (uint32_t u = 0; u < G; u++)
+              pass |= (uint32_t)(screen_u_f32(cal, ca8h, clb, cAL, cAH, xf[hb][w][gs + u]) < Kq) << u;
+            while (pass) {
+              const uint32_t u = __ffs(pass) - 1;
+              pass &= pass - 1;
+              const uint32_t y = eval_exact(c, xs[hb][w][gs + u]);
+              if (y < Kq - kScr4W) Kq = y + kScr4W;   // (y < m <= 2^32 - 1 - W: no wrap)
             }
-#pragma unroll
-            for (int q = 0; q < NPL; q++) K[q] = kq[w][q][lane];
+            kq[w][q][lane] = Kq;
           }
+#pragma unroll
+          for (int q = 0; q < NPL; q++) K[q] = kq[w][q][lane];
         }
         __syncwarp();
       }
@@ -1173,13 +1186,13 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
   }
 }
 
-template <int NPL, int PASSES, int MINB = 2, int G = 4>
+template <int NPL, int PASSES, int MINB = 2, int G = 4, int R = 1>
 static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int bps_of[2] = {0, 0};   // [gated]
   const int gi = p.landed ? 1 : 0;
   if (!bps_of[gi]) {
-    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true, G>, K1_THREADS, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false, G>, K1_THREADS, 0);
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true, G, R>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false, G, R>, K1_THREADS, 0);
     if (bps_of[gi] < 1) bps_of[gi] = 1;
   }
   const int blocks_per_sm = bps_of[gi];
@@ -1187,8 +1200,8 @@ static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int m
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true, G><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
-  else k1_minhash_scr4<NPL, PASSES, MINB, false, G><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true, G, R><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr4<NPL, PASSES, MINB, false, G, R><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
@@ -1367,7 +1380,8 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     else if (scr == 4) launch_s3<8, 1, 2>(b, sm_count, s, max_bps);
     else if (scr == 6) launch_s4<8, 1, 3>(b, sm_count, s, max_bps);   // (3 blocks per SM: diagnostic)
     else if (scr == 8) launch_s4<8, 1, 2, 4>(b, sm_count, s, max_bps);   // (4-shingle groups: diagnostic)
-    else launch_s4<8, 1, 2, 8>(b, sm_count, s, max_bps);
+    else if (scr == 10) launch_s4<8, 1, 2, 8, 1>(b, sm_count, s, max_bps);   // (resolution every chunk: diagnostic)
+    else launch_s4<8, 1, 2, 8, 2>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
     if (long_first) short_docs();
