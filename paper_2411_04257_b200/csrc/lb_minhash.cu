@@ -1249,18 +1249,22 @@ static int launch_t(const MinhashParams& p, int sm_count, cudaStream_t s, int ma
 // the tokens land in document order).  K1p1 counts long documents per 1024-document block;
 // K1p2 scans the counts of the preceding blocks and places each document with warp ballots.
 constexpr int kPartBlock = 1024;
-__device__ __forceinline__ bool is_long_doc(const MinhashParams& p, uint32_t d, uint32_t split_s) {
+__device__ __forceinline__ uint32_t doc_shingles(const MinhashParams& p, uint32_t d) {
   const uint64_t L = p.offsets[d + 1] - p.offsets[d];
-  const uint64_t S = L >= p.shingle_n ? L - p.shingle_n + 1 : 1;
-  return S >= split_s;
+  return (uint32_t)(L >= p.shingle_n ? L - p.shingle_n + 1 : 1);
 }
-__global__ void __launch_bounds__(kPartBlock) k1_partition_count(const MinhashParams p, uint32_t split_s) {
+// Three classes: short (S < split_s), long, and very long (S >= vlong_s; a subset of the long
+// list placed at its front, so the longest documents start first and the launch does not end on
+// a warp still walking one of them).  part_blk[b] = long | very long << 16 for block b.
+__global__ void __launch_bounds__(kPartBlock) k1_partition_count(const MinhashParams p, uint32_t split_s,
+                                                                 uint32_t vlong_s) {
   __shared__ uint32_t wsum[kPartBlock / 32];
   if (*p.err) return;
   const uint32_t di = blockIdx.x * kPartBlock + threadIdx.x;
-  const bool lg = di < p.n_docs && is_long_doc(p, p.doc0 + di, split_s);
-  const uint32_t bal = __ballot_sync(0xffffffffu, lg);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+  const uint32_t S = di < p.n_docs ? doc_shingles(p, p.doc0 + di) : 0;
+  const uint32_t bl = __ballot_sync(0xffffffffu, di < p.n_docs && S >= split_s);
+  const uint32_t bv = __ballot_sync(0xffffffffu, di < p.n_docs && S >= split_s && S >= vlong_s);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bl) | (__popc(bv) << 16);
   __syncthreads();
   if (threadIdx.x < 32) {
     uint32_t v = wsum[threadIdx.x];
@@ -1268,28 +1272,41 @@ __global__ void __launch_bounds__(kPartBlock) k1_partition_count(const MinhashPa
     if (threadIdx.x == 0) p.part_blk[blockIdx.x] = v;
   }
 }
-__global__ void __launch_bounds__(kPartBlock) k1_partition_place(const MinhashParams p, uint32_t split_s) {
+__global__ void __launch_bounds__(kPartBlock) k1_partition_place(const MinhashParams p, uint32_t split_s,
+                                                                 uint32_t vlong_s) {
   __shared__ uint32_t wl[kPartBlock / 32];
-  __shared__ uint32_t base_long;
+  __shared__ uint32_t base_long, base_vlong, tot_vlong;
   if (*p.err) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (w == 0) {   // long documents in the preceding blocks
-    uint32_t acc = 0;
-    for (uint32_t b = lane; b < blockIdx.x; b += 32) acc += p.part_blk[b];
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) base_long = acc;
+  if (w == 0) {   // long / very long documents in the preceding blocks; very long ones in all blocks
+    uint32_t acc = 0, accv = 0, totv = 0;
+    for (uint32_t b = lane; b < gridDim.x; b += 32) {
+      const uint32_t v = p.part_blk[b];
+      if (b < blockIdx.x) { acc += v & 0xFFFFu; accv += v >> 16; }
+      totv += v >> 16;
+    }
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      accv += __shfl_xor_sync(0xffffffffu, accv, o);
+      totv += __shfl_xor_sync(0xffffffffu, totv, o);
+    }
+    if (lane == 0) { base_long = acc; base_vlong = accv; tot_vlong = totv; }
   }
   const uint32_t di = blockIdx.x * kPartBlock + threadIdx.x;
   const bool in = di < p.n_docs;
-  const bool lg = in && is_long_doc(p, p.doc0 + di, split_s);
-  const uint32_t bal = __ballot_sync(0xffffffffu, lg);
-  if (lane == 0) wl[w] = __popc(bal);
+  const uint32_t S = in ? doc_shingles(p, p.doc0 + di) : 0;
+  const bool lg = in && S >= split_s, vl = lg && S >= vlong_s;
+  const uint32_t bl = __ballot_sync(0xffffffffu, lg), bv = __ballot_sync(0xffffffffu, vl);
+  if (lane == 0) wl[w] = __popc(bl) | (__popc(bv) << 16);
   __syncthreads();
-  uint32_t before = 0;                          // long documents of the earlier warps of the block
+  uint32_t before = 0;                          // long | very long << 16 of the earlier warps of the block
   for (int i = 0; i < w; i++) before += wl[i];
-  const uint32_t rank_long = base_long + before + __popc(bal & ((1u << lane) - 1));
+  const uint32_t lt = (1u << lane) - 1;
+  const uint32_t rank_long = base_long + (before & 0xFFFFu) + __popc(bl & lt);     // among all long
+  const uint32_t rank_vl = base_vlong + (before >> 16) + __popc(bv & lt);          // among very long
   if (in) {
-    if (lg) p.part_lists[(uint64_t)p.n_docs + rank_long] = p.doc0 + di;
+    if (vl) p.part_lists[(uint64_t)p.n_docs + rank_vl] = p.doc0 + di;
+    else if (lg) p.part_lists[(uint64_t)p.n_docs + tot_vlong + (rank_long - rank_vl)] = p.doc0 + di;
     else p.part_lists[di - rank_long] = p.doc0 + di;        // short rank = documents before - long before
   }
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kPartBlock - 1) {
@@ -1341,9 +1358,16 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
       const char* e = getenv("LSHBLOOM_K1_SPLIT_S");
       split_s = e ? (uint32_t)atoi(e) : 1024u;
     }
+    // very long documents first, except on landing-gated launches (the tokens land in document
+    // order, and a warp waits for its document's): LSHBLOOM_K1_VLONG_S shingles (0 = off)
+    static const uint32_t vlong_env = [] {
+      const char* e = getenv("LSHBLOOM_K1_VLONG_S");
+      return e ? (uint32_t)atoi(e) : 8192u;
+    }();
+    const uint32_t vlong_s = (p.landed || vlong_env == 0) ? 0xFFFFFFFFu : vlong_env;
     const unsigned pblocks = (p.n_docs + kPartBlock - 1) / kPartBlock;
-    k1_partition_count<<<pblocks, kPartBlock, 0, s>>>(p, split_s);
-    k1_partition_place<<<pblocks, kPartBlock, 0, s>>>(p, split_s);
+    k1_partition_count<<<pblocks, kPartBlock, 0, s>>>(p, split_s, vlong_s);
+    k1_partition_place<<<pblocks, kPartBlock, 0, s>>>(p, split_s, vlong_s);
     MinhashParams a = p, b = p;
     a.list = p.part_lists;
     a.list_n = p.part_counts;

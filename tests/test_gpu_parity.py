@@ -332,7 +332,7 @@ print("ok")
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
-@pytest.mark.parametrize("split", ["1", "300", "100000"])
+@pytest.mark.parametrize("split", ["1", "300", "100000", "300:2000", "1:1", "300:0"])
 def test_length_partitioned_k1(split):
     # 256 permutations: each K1 launch is split by shingle count into an exact-kernel part and a
     # screened-kernel part (lb_minhash.cu); every threshold must give the oracle's outputs,
@@ -357,7 +357,11 @@ for name, n in (("C4", 2000), ("C1", 1500)):
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    # "split:vlong": also the very-long class placed first (LSHBLOOM_K1_VLONG_S; 0 = off)
+    split, _, vlong = split.partition(":")
     env = dict(os.environ, LSHBLOOM_K1_SPLIT_S=split, PYTHONPATH=root)
+    if vlong:
+        env["LSHBLOOM_K1_VLONG_S"] = vlong
     env.pop("LSHBLOOM_K1", None)
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
