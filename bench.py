@@ -147,17 +147,23 @@ def workload(cfg, rank: int, n_docs: int):
     return off, tok, time.time() - t
 
 
-def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 1024):
-    """(total, on the exact kernel, on the screened kernel) evaluations: S_d x num_perm per
-    document, S_d = max(1, L_d - n + 1).  With 256 permutations the library runs documents of
-    >= split_s shingles on the screened kernel (lb_minhash.cu, LSHBLOOM_K1_SPLIT_S)."""
+def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 1024, prefix: int = 32):
+    """(total, exact-form, screened-form) evaluations: S_d x num_perm per document, S_d =
+    max(1, L_d - n + 1).  The library runs the FP32-screen kernel for 65-128 permutations and, with
+    256, for documents of >= split_s shingles (lb_minhash.cu, LSHBLOOM_K1_SPLIT_S); that kernel
+    evaluates each document's first `prefix` shingles exactly (LSHBLOOM_K1_PREFIX / _LPREFIX = one
+    32-shingle chunk) and screens the rest.  Everything else runs the exact kernel."""
     L = np.diff(off.astype(np.int64))
     S = np.where(L >= n, L - n + 1, 1)
     total = int(S.sum()) * num_perm
     if num_perm > 128:
-        long_ = int(S[S >= split_s].sum()) * num_perm
-        return total, total - long_, long_
-    return total, total, 0
+        scr_docs = S >= split_s
+    elif num_perm > 64:
+        scr_docs = np.ones(len(S), dtype=bool)
+    else:
+        return total, total, 0
+    screened = int(np.maximum(S[scr_docs] - prefix, 0).sum()) * num_perm
+    return total, total - screened, screened
 
 
 # K1 bounds per evaluation (tools/micro/pipe_micro.cu, profiles/r02h_microbench.txt +

@@ -18,6 +18,7 @@
 //   q = floor(S / P) = (S' + (S' >> 61)) >> 61,   y = low32(S - q P) = low32(S') - 1 + q.
 // Four 32x32->64 multiplies (the minimum for a 61x61-bit product; IMAD.WIDE issues at 1/4 rate)
 // plus ~8 ALU ops; tools/micro measured the per-opcode rates.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -1333,15 +1334,23 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     const char* e = getenv("LSHBLOOM_K1");
     mode = !e ? 2 : (e[0] == 'e' ? 0 : (e[0] == 'h' ? 3 : 1));
   }
-  // 65-128 permutations (C1, C2, C5): the FP64-screen kernel with the documents' first 32
-  // shingles evaluated exactly (where candidates are dense) unless the caller runs K1 beside the
+  // 65-128 permutations (C1, C2, C5): the screen kernel (FP32 since round 2; LSHBLOOM_K1_SCR=4 the
+  // FP64 one) with the documents' first 32 shingles evaluated exactly (where candidates are dense).
+  // Round 1 kept the exact kernel when the caller runs K1 beside the
   // random-access Bloom kernels (L2-resident filters), whose latency-bound kernels need the SM room
   // the 92-register exact kernel leaves (C2 step 18.9 vs 19.4 ms with the screen at 2 blocks per
   // SM).  K1 alone on C2 batches: 14.1 vs 17.1 ms; C5 fused sweep step 46.6 vs 53.3 ms per 2M
   // documents (prefix 0 / 1 / 2 / 3 / 4 chunks: 18.0 / 14.1 / 14.8 / 15.7 / 16.8 ms on C2).
   // LSHBLOOM_K1=exact keeps the exact kernel everywhere, =hyb forces the screen.
-  if (npl == 4 && (mode == 3 || (mode == 2 && !p.beside_random_bloom))) {
+  //
+  // Round 2: with the FP32 screen this holds beside the random-access kernels too once K1 is capped
+  // at one block (8 warps) per SM, which leaves them the registers and warp slots the exact
+  // kernel's two blocks took: C2 step 18.9 -> 17.9 ms (2 / 3 blocks: 19.2 / 20.7 ms; the exact
+  // kernel at one block: 19.1 ms).  LSHBLOOM_K1_SCR_BPS overrides the cap.
+  if (npl == 4 && (mode == 3 || mode == 2)) {
     static const uint32_t pre = [] { const char* e = getenv("LSHBLOOM_K1_PREFIX"); return e ? (uint32_t)atoi(e) : 1u; }();
+    static const int scr_bps = [] { const char* e = getenv("LSHBLOOM_K1_SCR_BPS"); return e ? atoi(e) : 1; }();
+    if (mode == 2 && p.beside_random_bloom && max_bps > 0) max_bps = std::min(max_bps, scr_bps);
     MinhashParams q = p;
     q.exact_prefix = pre;
     if (k1_scr_choice() == 4) return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
