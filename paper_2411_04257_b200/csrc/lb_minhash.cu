@@ -137,32 +137,55 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ bool await_tokens_impl(const uint32_t* landed, uint32_t land_log2, uint64_t tok_total,
-                                              const int* gate, ErrState* es, uint64_t o1) {
-  const uint64_t r32 = (o1 + 31) & ~(uint64_t)31, end = tok_total < r32 ? tok_total : r32;
-  const uint32_t need = (uint32_t)((end + (1ull << land_log2) - 1) >> land_log2);
-  if (ld_acquire_u32(landed) >= need) return true;
+// `known`: the largest counter value already acquired.  The acquire load compiles to a strong
+// load plus an L1 invalidation (CCTL.IVALL), which also evicts other warps' L1-resident lines;
+// once a value is acquired, the pieces it covers stay visible, so documents within it need no new
+// load.  The polling loop and its error path are a separate (not inlined) function.
+__device__ __noinline__ uint32_t await_tokens_slow(const uint32_t* landed, const int* gate, ErrState* es,
+                                                   uint32_t need) {
+  if (*(volatile const int*)&es->flags & 2) return 0;      // an earlier wait timed out: fail fast
+  uint32_t v = ld_acquire_u32(landed);
+  if (v >= need) return v;
   const uint64_t t0 = globaltimer_ns();
   for (;;) {
     __nanosleep(256);
-    if (ld_acquire_u32(landed) >= need) return true;
-    if (*(volatile const int*)gate) return false;             // the batch was rejected meanwhile
+    v = ld_acquire_u32(landed);
+    if (v >= need) return v;
+    if (*(volatile const int*)gate) return 0;                 // the batch was rejected meanwhile
     if (globaltimer_ns() - t0 > kLandTimeoutNs) {
       atomicOr(&es->flags, 2);
       atomicExch(&es->pad, 1);
-      return false;
+      return 0;
     }
   }
 }
-__device__ __forceinline__ bool await_tokens(const MinhashParams& p, uint64_t o1) {
-  return await_tokens_impl(p.landed, p.land_log2, p.tok_total, p.err, p.err_state, o1);
+__device__ __forceinline__ bool await_tokens_impl(const uint32_t* landed, uint32_t land_log2, uint64_t tok_total,
+                                              const int* gate, ErrState* es, uint64_t o1, uint32_t& known) {
+  const uint64_t r32 = (o1 + 31) & ~(uint64_t)31, end = tok_total < r32 ? tok_total : r32;
+  const uint32_t need = (uint32_t)((end + (1ull << land_log2) - 1) >> land_log2);
+  if (known >= need) return true;
+  const uint32_t v = await_tokens_slow(landed, gate, es, need);
+  if (v < need) return false;
+  known = v;
+  return true;
 }
-// Per-warp form: lane 0 waits, the verdict is broadcast.
-__device__ __forceinline__ bool warp_await_tokens(const MinhashParams& p, uint32_t d, int lane) {
+__device__ __forceinline__ bool await_tokens(const MinhashParams& p, uint64_t o1, uint32_t& known) {
+  return await_tokens_impl(p.landed, p.land_log2, p.tok_total, p.err, p.err_state, o1, known);
+}
+// Warp-uniform form: every lane computes the same `need` and holds the same `known`, and the
+// waiting lane's counter value is broadcast, so the branch is uniform by construction (with the
+// verdict of lane 0 alone, ptxas moved the FP32-screen loop's uniform address and loop arithmetic
+// from the uniform datapath onto the fma pipe and dropped operand-reuse flags: C3 K1 +3.5 ms).
+__device__ __forceinline__ bool warp_await_tokens_u(const MinhashParams& p, uint32_t d, uint32_t& known) {
   if (!p.landed) return true;
-  int ok = 1;
-  if (lane == 0) ok = await_tokens(p, p.offsets[d + 1]);
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+  const uint64_t o1 = p.offsets[d + 1];
+  const uint64_t r32 = (o1 + 31) & ~(uint64_t)31, end = p.tok_total < r32 ? p.tok_total : r32;
+  const uint32_t need = (uint32_t)((end + (1ull << p.land_log2) - 1) >> p.land_log2);
+  if (known >= need) return true;
+  const uint32_t v = __shfl_sync(0xffffffffu, await_tokens_slow(p.landed, p.err, p.err_state, need), 0);
+  if (v < need) return false;
+  known = v;
+  return true;
 }
 
 __device__ __forceinline__ XLimbs make_limbs(uint64_t fp) {
@@ -187,6 +210,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashPara
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (*p.err) return;
   const uint64_t tpol = l2_evict_first_policy();
+  uint32_t land_known = 0;   // landing counter value already acquired (gated launches)
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
@@ -197,7 +221,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash(const MinhashPara
     di = __shfl_sync(0xffffffffu, di, 0);
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
-    if (GATED && !warp_await_tokens(p, d, lane)) break;
+    if (GATED && !warp_await_tokens_u(p, d, land_known)) continue;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -368,6 +392,7 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
   if (*p.err) return;
   if (p.block_gate && p.list && ((*p.list_n < p.block_gate) != BLOCKDOC)) return;   // the other mode runs
   const uint64_t tpol = l2_evict_first_policy();
+  uint32_t land_known = 0;   // landing counter value already acquired (gated launches)
   PermCoef c[NPL];
 #pragma unroll
   for (int q = 0; q < NPL; q++) c[q] = p.coef[lane + 32 * q];
@@ -381,7 +406,7 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
       if (threadIdx.x == 0) {   // (the whole block takes the gate's verdict: no barrier divergence)
         uint32_t v = atomicAdd(p.counter, 1u);
         const uint32_t nd = p.list ? *p.list_n : p.n_docs;
-        if (GATED && v < nd && !await_tokens(p, p.offsets[(p.list ? p.list[v] : p.doc0 + v) + 1]))
+        if (GATED && v < nd && !await_tokens(p, p.offsets[(p.list ? p.list[v] : p.doc0 + v) + 1], land_known))
           v = 0xFFFFFFFFu;
         s_doc = v;
       }
@@ -395,7 +420,7 @@ __global__ void __launch_bounds__(K1_THREADS, BLOCKDOC ? 2 : LB_K1S_MINB) k1_min
     }
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
-    if (GATED && !BLOCKDOC && !warp_await_tokens(p, d, lane)) break;
+    if (GATED && !BLOCKDOC && !warp_await_tokens_u(p, d, land_known)) continue;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -589,6 +614,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr2(const Minhas
   if (*p.err) return;
   if (p.block_gate && p.list && *p.list_n < p.block_gate) return;   // the block-per-document kernel runs
   const uint64_t tpol = l2_evict_first_policy();
+  uint32_t land_known = 0;   // landing counter value already acquired (gated launches)
   const uint32_t sh29 = p.sh29;
 
   for (;;) {
@@ -597,7 +623,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr2(const Minhas
     di = __shfl_sync(0xffffffffu, di, 0);
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
-    if (GATED && !warp_await_tokens(p, d, lane)) break;
+    if (GATED && !warp_await_tokens_u(p, d, land_known)) continue;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -786,6 +812,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
   if (*p.err) return;
   if (p.block_gate && p.list && *p.list_n < p.block_gate) return;   // the block-per-document kernel runs
   const uint64_t tpol = l2_evict_first_policy();
+  uint32_t land_known = 0;   // landing counter value already acquired (gated launches)
 
   for (;;) {
     uint32_t di = 0;
@@ -793,7 +820,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr3(const Minhas
     di = __shfl_sync(0xffffffffu, di, 0);
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
-    if (GATED && !warp_await_tokens(p, d, lane)) break;
+    if (GATED && !warp_await_tokens_u(p, d, land_known)) continue;
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -985,10 +1012,16 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
   __shared__ XLimbsS xf[R][K1_WARPS][32];    // screen limbs
   __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
   __shared__ uint32_t kq[K1_WARPS][NPL][32];  // thresholds while flagged groups are resolved
+  __shared__ PermCoef cs[32 * NPL * PASSES];   // the coefficient table (exact evaluations read it
+                                              // by permutation; shared memory is immune to the
+                                              // L1 invalidations of gated launches)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < 32 * NPL * PASSES; i += K1_THREADS) cs[i] = p.coef[i];
+  __syncthreads();
   if (*p.err) return;
   if (p.block_gate && p.list && *p.list_n < p.block_gate) return;   // the block-per-document kernel runs
   const uint64_t tpol = l2_evict_first_policy();
+  uint32_t land_known = 0;   // landing counter value already acquired (gated launches)
 
   for (;;) {
     uint32_t di = 0;
@@ -996,7 +1029,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
     di = __shfl_sync(0xffffffffu, di, 0);
     if (di >= (p.list ? *p.list_n : p.n_docs)) break;
     const uint32_t d = p.list ? p.list[di] : p.doc0 + di;
-    if (GATED && !warp_await_tokens(p, d, lane)) break;
+    if (GATED && !warp_await_tokens_u(p, d, land_known)) continue;   // (rejected batch: the rest fail fast)
     const uint64_t o0 = p.offsets[d];
     const uint64_t L = p.offsets[d + 1] - o0;
     LB_ASSERT(L >= 1 && o0 >= p.tok_base);
@@ -1012,7 +1045,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
       float AL[NPL], AH[NPL];
 #pragma unroll
       for (int q = 0; q < NPL; q++) {
-        const PermCoef c = p.coef[pm0 + 32 * q];             // a = a1 2^31 + a0
+        const PermCoef c = cs[pm0 + 32 * q];             // a = a1 2^31 + a0
         al[q] = c.a0 | (c.a1 << 31);
         a8h[q] = (c.a1 >> 1) << 3;
         lb[q] = c.b0 + kScr4D;
@@ -1076,7 +1109,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
           const XLimbs x0 = xs[bf][w][0];
 #pragma unroll
           for (int q = 0; q < NPL; q++) {
-            if (s0 == 0) K[q] = eval_exact(p.coef[pm0 + 32 * q], x0);   // (the raw minimum, for now)
+            if (s0 == 0) K[q] = eval_exact(cs[pm0 + 32 * q], x0);   // (the raw minimum, for now)
             big |= K[q] > 0xFFFFFFFFu - kScr4W;               // m + W would wrap
           }
           if (s0 == 0) j = 1;
@@ -1090,7 +1123,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
           for (; j < cnt; j++) {
             const XLimbs xv = xs[bf][w][j];
 #pragma unroll
-            for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(p.coef[pm0 + 32 * q], xv));
+            for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(cs[pm0 + 32 * q], xv));
           }
         } else {
           // groups of 4 shingles from j0: bit g of mask[q] = some u of group g is below K[q]
@@ -1116,7 +1149,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
             const XLimbs xv = xs[bf][w][j];
 #pragma unroll
             for (int q = 0; q < NPL; q++) {
-              const uint32_t y = eval_exact(p.coef[pm0 + 32 * q], xv);
+              const uint32_t y = eval_exact(cs[pm0 + 32 * q], xv);
               if (y < K[q] - kScr4W) K[q] = y + kScr4W;
             }
           }
@@ -1141,7 +1174,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
             cm &= cm - 1;
             const uint32_t hb = R == 2 ? ((bit >> 2) & 1) : 0;          // the chunk's buffer
             const uint32_t q = bit >> 3, gs = (hb ? j0s1 : j0s0) + G * (R == 2 ? (bit & 3) : (bit & 7));
-            const PermCoef c = p.coef[pm0 + 32 * q];
+            const PermCoef c = cs[pm0 + 32 * q];
             const uint32_t cal = c.a0 | (c.a1 << 31), ca8h = (c.a1 >> 1) << 3, clb = c.b0 + kScr4D;
             const float cAL = __uint2float_rn(cal), cAH = __uint2float_rn(c.a1 >> 1);
             uint32_t Kq = kq[w][q][lane];
