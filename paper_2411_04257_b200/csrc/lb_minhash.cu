@@ -1005,13 +1005,15 @@ __device__ __forceinline__ uint32_t screen_u_f32(uint32_t al, uint32_t a8h, uint
   return t + hb;
 }
 
-template <int NPL, int PASSES, int MINB = 2, bool GATED = false, int G = 4, int R = 1>
+template <int NPL, int PASSES, int MINB = 2, bool GATED = false, int G = 4, int R = 1, bool BAL = true>
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const MinhashParams p) {
   static_assert(R == 1 || (R == 2 && G == 8), "deferred resolution packs two chunks' 4 groups");
   __shared__ XLimbs xs[R][K1_WARPS][32];     // exact-evaluation limbs (R chunks)
   __shared__ XLimbsS xf[R][K1_WARPS][32];    // screen limbs
   __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
   __shared__ uint32_t kq[K1_WARPS][NPL][32];  // thresholds while flagged groups are resolved
+  constexpr uint32_t kRQ = 512;                 // balanced-resolution queue per warp (the rest per lane)
+  __shared__ uint16_t rq[BAL ? K1_WARPS : 1][BAL ? kRQ : 1];   // flagged (lane, bit) items
   __shared__ PermCoef cs[32 * NPL * PASSES];   // the coefficient table (exact evaluations read it
                                               // by permutation; shared memory is immune to the
                                               // L1 invalidations of gated launches)
@@ -1169,6 +1171,48 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
         if ((R == 1 || bf == 1 || s0 + 32 >= S) && __any_sync(0xffffffffu, cm != 0)) {
 #pragma unroll
           for (int q = 0; q < NPL; q++) kq[w][q][lane] = K[q];
+          if (BAL) {
+            // (128 permutations: abstract-length documents have many flagged groups per chunk,
+            // unevenly spread over the lanes -- C5 K1 28.3 -> 26.9 ms per 2M documents, C2 14.2 ->
+            // 13.5 ms; with 256 the long documents' sparse flags favour the per-lane walk below,
+            // C3 63.4 vs 65.8 ms)
+            // the warp's flagged (lane, permutation, group) items, load-balanced over the lanes:
+            // each lane's items go to a shared queue at its prefix-sum offset and lane l takes items
+            // l, l + 32, ... (rounds = ceil(items / 32) instead of the largest per-lane count);
+            // thresholds live in kq meanwhile, lowered with shared-memory atomicMin
+            const uint32_t cnt = (uint32_t)__popcll(cm);
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += t;
+            }
+            const uint32_t total = min(kRQ, __shfl_sync(0xffffffffu, incl, 31));
+            for (uint32_t off = incl - cnt; cm && off < kRQ; cm &= cm - 1) rq[w][off++] = (uint16_t)((lane << 8) | (__ffsll(cm) - 1));
+            __syncwarp();
+            for (uint32_t it = lane; it < total; it += 32) {
+              const uint32_t item = rq[w][it], ol = item >> 8, bit = item & 0xFFu;
+              const uint32_t hb = R == 2 ? ((bit >> 2) & 1) : 0;          // the chunk's buffer
+              const uint32_t q = bit >> 3, gs = (hb ? j0s1 : j0s0) + G * (R == 2 ? (bit & 3) : (bit & 7));
+              const PermCoef c = cs[pass * 32 * NPL + ol + 32 * q];
+              const uint32_t cal = c.a0 | (c.a1 << 31), ca8h = (c.a1 >> 1) << 3, clb = c.b0 + kScr4D;
+              const float cAL = __uint2float_rn(cal), cAH = __uint2float_rn(c.a1 >> 1);
+              const uint32_t Kq = *(volatile uint32_t*)&kq[w][q][ol];   // (stale only admits more)
+              uint32_t pass_bits = 0;
+#pragma unroll
+              for (uint32_t u = 0; u < G; u++)
+                pass_bits |= (uint32_t)(screen_u_f32(cal, ca8h, clb, cAL, cAH, xf[hb][w][gs + u]) < Kq) << u;
+              uint32_t ymin = 0xFFFFFFFFu;
+              while (pass_bits) {
+                const uint32_t u = __ffs(pass_bits) - 1;
+                pass_bits &= pass_bits - 1;
+                ymin = min(ymin, eval_exact(c, xs[hb][w][gs + u]));
+              }
+              if (ymin < Kq - kScr4W) atomicMin(&kq[w][q][ol], ymin + kScr4W);   // (y < m: no wrap)
+            }
+            __syncwarp();
+          }
+          {   // items beyond the queue (or all of them without BAL): each lane its own
           while (cm) {
             const uint32_t bit = __ffsll(cm) - 1;
             cm &= cm - 1;
@@ -1190,6 +1234,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
               if (y < Kq - kScr4W) Kq = y + kScr4W;   // (y < m <= 2^32 - 1 - W: no wrap)
             }
             kq[w][q][lane] = Kq;
+          }
           }
 #pragma unroll
           for (int q = 0; q < NPL; q++) K[q] = kq[w][q][lane];
@@ -1220,13 +1265,13 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
   }
 }
 
-template <int NPL, int PASSES, int MINB = 2, int G = 4, int R = 1>
+template <int NPL, int PASSES, int MINB = 2, int G = 4, int R = 1, bool BAL = true>
 static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int max_bps) {
   static int bps_of[2] = {0, 0};   // [gated]
   const int gi = p.landed ? 1 : 0;
   if (!bps_of[gi]) {
-    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true, G, R>, K1_THREADS, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false, G, R>, K1_THREADS, 0);
+    if (gi) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, true, G, R, BAL>, K1_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps_of[gi], k1_minhash_scr4<NPL, PASSES, MINB, false, G, R, BAL>, K1_THREADS, 0);
     if (bps_of[gi] < 1) bps_of[gi] = 1;
   }
   const int blocks_per_sm = bps_of[gi];
@@ -1234,8 +1279,8 @@ static int launch_s4(const MinhashParams& p, int sm_count, cudaStream_t s, int m
   const int bps = (max_bps > 0 && max_bps < blocks_per_sm) ? max_bps : blocks_per_sm;
   uint64_t grid = (uint64_t)sm_count * bps;
   if (want < grid) grid = want ? want : 1;
-  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true, G, R><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
-  else k1_minhash_scr4<NPL, PASSES, MINB, false, G, R><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  if (p.landed) k1_minhash_scr4<NPL, PASSES, MINB, true, G, R, BAL><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
+  else k1_minhash_scr4<NPL, PASSES, MINB, false, G, R, BAL><<<(unsigned)grid, K1_THREADS, 0, s>>>(p);
   return 1;
 }
 
@@ -1389,6 +1434,7 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     if (k1_scr_choice() == 4) return launch_s3<4, 1, 3>(q, sm_count, s, max_bps);
     if (k1_scr_choice() == 7) return launch_s4<4, 1, 2>(q, sm_count, s, max_bps);
     if (k1_scr_choice() == 9) return launch_s4<4, 1, 3, 8>(q, sm_count, s, max_bps);
+    if (k1_scr_choice() == 11) return launch_s4<4, 1, 3, 4, 1, false>(q, sm_count, s, max_bps);   // (per-lane)
     return launch_s4<4, 1, 3>(q, sm_count, s, max_bps);
   }
   if (mode == 2 && npl == 8 && p.part_lists && p.n_docs > 0) {
@@ -1447,7 +1493,8 @@ int launch_minhash(const MinhashParams& p, int npl, int sm_count, cudaStream_t s
     else if (scr == 6) launch_s4<8, 1, 3>(b, sm_count, s, max_bps);   // (3 blocks per SM: diagnostic)
     else if (scr == 8) launch_s4<8, 1, 2, 4>(b, sm_count, s, max_bps);   // (4-shingle groups: diagnostic)
     else if (scr == 10) launch_s4<8, 1, 2, 8, 1>(b, sm_count, s, max_bps);   // (resolution every chunk: diagnostic)
-    else launch_s4<8, 1, 2, 8, 2>(b, sm_count, s, max_bps);
+    else if (scr == 11) launch_s4<8, 1, 2, 8, 2, true>(b, sm_count, s, max_bps);   // (balanced resolution: diagnostic)
+    else launch_s4<8, 1, 2, 8, 2, false>(b, sm_count, s, max_bps);
     cudaMemsetAsync(p.counter, 0, 4, s);
     launch_s<8, true>(b, sm_count, s, max_bps);
     if (long_first) short_docs();

@@ -287,13 +287,14 @@ def test_many_chunks_short_docs(on_device):
     assert (u64(idx.band_hashes(*args)) == bh).all()
 
 
-@pytest.mark.parametrize("mode", ["exact", "screened", "hyb:0", "hyb:1", "hyb:3", "scr:2", "scr:3", "scr:4", "scr:8", "scr:10", "scr:4+hyb:1"])
+@pytest.mark.parametrize("mode", ["exact", "screened", "hyb:0", "hyb:1", "hyb:3", "scr:2", "scr:3", "scr:4", "scr:8", "scr:10", "scr:11", "scr:4+hyb:1"])
 def test_both_minhash_kernels(mode):
     # exact / screened: LSHBLOOM_K1 for every launch; hyb:k the FP64-screen kernel with a k-chunk
     # exact prefix for 128 permutations; scr:k the long-document kernel of the 256-permutation
     # split (2: integer screen, 3: FP64 screen in two passes, 4: FP64 screen in one pass; default:
     # the FP32 screen in 8-shingle groups resolved every second chunk, 10: resolved every chunk,
-    # 8: in 4-shingle groups as the 128-permutation hyb batches run it unless scr:4+hyb)
+    # 8: in 4-shingle groups as the 128-permutation hyb batches run it unless scr:4+hyb; 11: the
+    # other resolution (balanced over the lanes for 256 permutations, per lane for 128))
     # run in a subprocess: the kernel choice is read once per process from LSHBLOOM_K1
     import os
     import subprocess
