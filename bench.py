@@ -147,7 +147,7 @@ def workload(cfg, rank: int, n_docs: int):
     return off, tok, time.time() - t
 
 
-def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 1024, prefix: int = 32):
+def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 128, prefix: int = 32):
     """(total, exact-form, screened-form) evaluations: S_d x num_perm per document, S_d =
     max(1, L_d - n + 1).  The library runs the FP32-screen kernel for 65-128 permutations and, with
     256, for documents of >= split_s shingles (lb_minhash.cu, LSHBLOOM_K1_SPLIT_S); that kernel
