@@ -1001,7 +1001,10 @@ __device__ __forceinline__ uint32_t screen_u_f32(uint32_t al, uint32_t a8h, uint
   uint32_t t, hb;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(al), "r"(x.xl), "r"(lb));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a8h), "r"(x.xh), "r"(t));
-  asm("shl.b32 %0, %1, 11;" : "=r"(hb) : "r"(__float_as_uint(r2)));
+  // bits << 11 as a funnel shift ({bits, 0} << 11, high word): ptxas then fuses it with the add
+  // into LEA.HI on the ALU pipe; a plain shl + add became IMAD (x 2048 + t) on the fma pipe -- the
+  // loop's bottleneck -- for 7 of every 8 evaluations (4.9 instead of 4.0 fma-pipe ops each)
+  asm("shf.l.wrap.b32 %0, %1, %2, 11;" : "=r"(hb) : "r"(0u), "r"(__float_as_uint(r2)));
   return t + hb;
 }
 
