@@ -635,7 +635,10 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
         if (!((first >> q) & 1) || ((joined >> q) & 1)) set_before = e_find_min(etab, gl) < doc;
         if (!set_before) red_or_keep(p.miss + doc, bitj, pol_keep);
       }
-      __syncthreads();                                       // every table read done
+      // Every table read done.  This is also the iteration's last barrier: meta[] of the next
+      // stages was published by the barriers above, and the next window's first table write comes
+      // after its own first barrier, which every thread reaches only after emptying its entries.
+      __syncthreads();
       if (touched) {                                         // empty what this thread filled
 #pragma unroll
         for (int q = 0; q < kSweepRPT; q++) {
@@ -646,7 +649,6 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
           etab[es[q]] = kEEmpty;
         }
       }
-      // (the next window's inserts come after its first barrier, so no barrier is needed here)
     } else {
       // ---- a bin beyond kSweepCapReg records: records streamed from global memory, earliest
       // setters in this CTA's direct-mapped global array (one entry per window position)
@@ -678,10 +680,11 @@ __global__ void __launch_bounds__(kSweepThreads, 4) k8_sweep(const SweepParams p
         const uint32_t gl = (uint32_t)(rr >> 32), doc = (uint32_t)rr;
         if (!(__ldcg(eg + gl) < doc)) atomicOr((unsigned long long*)(p.miss + doc), (unsigned long long)bitj);
       }
-      __syncthreads();
+      __syncthreads();                                       // eg[] reads done before the next reset
     }
+    // (no barrier here: thread 0 writes meta[fill] at the top of the next iteration only after
+    // every thread has read meta[st] -- they all passed this window's barriers since)
     st = st + 1 == S ? 0 : st + 1;
-    __syncthreads();                                         // meta[fill] published before it is read
   }
   if (tid == 0) bulk_wait_all();
 }
@@ -785,9 +788,10 @@ SweepLaunch sweep_launch_cfg(int sm_count, uint32_t wb) {
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k8_sweep, kSweepThreads, c.smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
-  // K8 is bound by its per-window barrier phases, not by HBM latency: more resident CTAs help
-  // (C5 geometry, 16 KB windows: 4 per SM 29.9 ms vs 2 per SM 36.1 ms for K7b + K8), deeper
-  // pipelines do not (2 / 3 / 4 stages within 0.1 ms)
+  // K8 is bound by its per-window barrier phases, not by HBM latency: more resident CTAs help up
+  // to the three per SM the 16 KB windows allow (C5: 2 per SM 36.1 ms for K7b + K8; a staging
+  // layout that fitted four was slower, 40.4 vs 36.6 ms per Bloom stage), deeper pipelines do
+  // not (2 / 3 / 4 stages within 0.1 ms)
   if (env_ctas > 0 && env_ctas < per_sm) per_sm = env_ctas;
   c.grid = sm_count * per_sm;
   return c;
