@@ -994,13 +994,30 @@ struct __align__(16) XLimbsS {                 // shingle x for the FP32 screen
   uint32_t xl, xh;                             // x mod 2^32, x >> 32
   float XL, XH;                                // fl(xl) 2^-29, fl(xh) 2^-29
 };
+// SPLIT: both products take the magic addend as an immediate (two 1-cycle FFMA instead of a 1- and a
+// 2-cycle one) and their bit patterns are added on the ALU: bits(r1) + bits(r2) = 2 bits(1.5 2^34) +
+// (the two rounded products) / 2^11, and 2 bits(1.5 2^34) << 11 = 0 (mod 2^32) (bits(1.5 2^34) = 0x50C00000),
+// so (bits(r1) + bits(r2)) << 11 = the same Hc with the same two roundings (|Hc - H| <= 3074 still holds: each sum
+// lies in [1.5 2^34, 1.75 2^34), ulp 2^11).  One fma-pipe cycle less, one ALU instruction more.
+#ifndef LB_SCR4_SPLITQ
+#define LB_SCR4_SPLITQ 0   // permutation slots per lane (of NPL) screened in the split form
+#endif
 __device__ __forceinline__ uint32_t screen_u_f32(uint32_t al, uint32_t a8h, uint32_t lb, float AL, float AH,
-                                                 const XLimbsS& x) {
+                                                 const XLimbsS& x, const bool SPLIT = false) {
   const float r1 = __fmaf_rn(AL, x.XH, kScr4Magic);
-  const float r2 = __fmaf_rn(AH, x.XL, r1);
+  float r2;
   uint32_t t, hb;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(al), "r"(x.xl), "r"(lb));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a8h), "r"(x.xh), "r"(t));
+  if (SPLIT) {
+    r2 = __fmaf_rn(AH, x.XL, kScr4Magic);
+    // (two funnel-shift-adds: a plain add of the bit patterns became IMAD.IADD on the fma pipe)
+    uint32_t hb1;
+    asm("shf.l.wrap.b32 %0, %1, %2, 11;" : "=r"(hb1) : "r"(0u), "r"(__float_as_uint(r1)));
+    asm("shf.l.wrap.b32 %0, %1, %2, 11;" : "=r"(hb) : "r"(0u), "r"(__float_as_uint(r2)));
+    return (t + hb1) + hb;
+  }
+  r2 = __fmaf_rn(AH, x.XL, r1);
   // bits << 11 as a funnel shift ({bits, 0} << 11, high word): ptxas then fuses it with the add
   // into LEA.HI on the ALU pipe; a plain shl + add became IMAD (x 2048 + t) on the fma pipe -- the
   // loop's bottleneck -- for 7 of every 8 evaluations (4.9 instead of 4.0 fma-pipe ops each)
@@ -1145,7 +1162,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
             for (int q = 0; q < NPL; q++) {
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
-              for (int u = 0; u < G; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u]));
+              for (int u = 0; u < G; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u], q < LB_SCR4_SPLITQ));
               if (mn < K[q]) mask[q] |= 1u << g;
             }
           }
