@@ -1156,6 +1156,9 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
           uint32_t g = 0;
           for (; j + G <= cnt; j += G, g++) {
             XLimbsS xv[G];
+#ifndef LB_SCR4_SEL_OR
+            const uint32_t gbit = 1u << g;
+#endif
 #pragma unroll
             for (int u = 0; u < G; u++) xv[u] = xf[bf][w][j + u];
 #pragma unroll
@@ -1163,7 +1166,11 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
               for (int u = 0; u < G; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u], q < LB_SCR4_SPLITQ));
+#ifndef LB_SCR4_SEL_OR
+              asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(mask[q]) : "r"(mn), "r"(K[q]), "r"(gbit));
+#else
               if (mn < K[q]) mask[q] |= 1u << g;
+#endif
             }
           }
           // the chunk's last (cnt - j0) mod G shingles: exactly (warp-uniform)
