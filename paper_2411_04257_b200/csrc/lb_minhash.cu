@@ -1148,17 +1148,18 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
             for (int q = 0; q < NPL; q++) K[q] = min(K[q], eval_exact(cs[pm0 + 32 * q], xv));
           }
         } else {
-          // groups of 4 shingles from j0: bit g of mask[q] = some u of group g is below K[q]
+          // groups of G shingles from j0: a flag per (slot q, group g) = some u of the group is below K[q]
           if (bf) j0s1 = j; else j0s0 = j;
-          uint32_t mask[NPL];
-#pragma unroll
-          for (int q = 0; q < NPL; q++) mask[q] = 0;
-          uint32_t g = 0;
-          for (; j + G <= cnt; j += G, g++) {
+          // the flag of (slot q, group g) goes straight into cm (bit 8 q + 4 bf + g) with a predicated
+          // OR of a warp-uniform bit (setp + @p or -> ISETP + @P LOP3; `if (mn < K) mask[q] |= bit` on
+          // per-slot mask registers compiled to ISETP + SEL + LOP3, a combine after the loop, and --
+          // the registers gone -- eight I2FP per group rematerialising AL[]): the loop is issue-bound,
+          // 404 -> 386 instructions per 64 evaluations, C3 K1 alone 60.4 -> 57.0 ms
+          uint32_t cml = 0, cmh = 0;
+          uint32_t gb0 = R == 2 ? (bf ? 16u : 1u) : 1u;   // 1 << (4 bf + g)
+          for (; j + G <= cnt; j += G, gb0 <<= 1) {
             XLimbsS xv[G];
-#ifndef LB_SCR4_SEL_OR
-            const uint32_t gbit = 1u << g;
-#endif
+            const uint32_t gb[4] = {gb0, gb0 << 8, gb0 << 16, gb0 << 24};
 #pragma unroll
             for (int u = 0; u < G; u++) xv[u] = xf[bf][w][j + u];
 #pragma unroll
@@ -1166,13 +1167,11 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
               uint32_t mn = 0xFFFFFFFFu;
 #pragma unroll
               for (int u = 0; u < G; u++) mn = min(mn, screen_u_f32(al[q], a8h[q], lb[q], AL[q], AH[q], xv[u], q < LB_SCR4_SPLITQ));
-#ifndef LB_SCR4_SEL_OR
-              asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(mask[q]) : "r"(mn), "r"(K[q]), "r"(gbit));
-#else
-              if (mn < K[q]) mask[q] |= 1u << g;
-#endif
+              if (q < 4) asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(cml) : "r"(mn), "r"(K[q]), "r"(gb[q & 3]));
+              else asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(cmh) : "r"(mn), "r"(K[q]), "r"(gb[q & 3]));
             }
           }
+          cm |= ((uint64_t)cmh << 32) | cml;
           // the chunk's last (cnt - j0) mod G shingles: exactly (warp-uniform)
           for (; j < cnt; j++) {
             const XLimbs xv = xs[bf][w][j];
@@ -1182,8 +1181,6 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
               if (y < K[q] - kScr4W) K[q] = y + kScr4W;
             }
           }
-#pragma unroll
-          for (int q = 0; q < NPL; q++) cm |= (uint64_t)mask[q] << (8 * q + (R == 2 ? 4 * bf : 0));
         }
         // exact evaluation of the flagged groups (every chunk, or with R = 2 every second chunk and
         // the last: a chunk's flags wait in cm while the next chunk is screened against the older
