@@ -177,10 +177,10 @@ def minhash_evals(off: np.ndarray, num_perm: int, n: int = 5, split_s: int = 128
 K1_EVALS_PER_CLK_SMSP = {"exact": 2.0, "screened": 32.0 / 7.0}
 
 
-def k1_peak(evals, f_hz: float, sms: int = 148):
+def k1_peak(evals, f_hz: float, sms: int = 148, screened: float | None = None):
     """Evaluation-weighted bound (Geval/s) of K1 for a batch split over the two kernels."""
     total, ex, sc = evals
-    t = (ex / K1_EVALS_PER_CLK_SMSP["exact"] + sc / K1_EVALS_PER_CLK_SMSP["screened"]) / (sms * 4 * f_hz)
+    t = (ex / K1_EVALS_PER_CLK_SMSP["exact"] + sc / (screened or K1_EVALS_PER_CLK_SMSP["screened"])) / (sms * 4 * f_hz)
     return total / t
 
 
@@ -609,6 +609,10 @@ def main():
                                "warp-evaluation), "
                                "weighted by evaluations" % (peak_src, f_max / 1e6),
                 "frac_of_exact_form_bound": (achieved / (2.0 * 148 * 4 * f_max)) if achieved else None,
+                # a stricter reading of the screened bound: with operand reuse the 3-register FFMA also
+                # issues at ~1/clk (profiles/r02v_reuse_micro_and_land.log), i.e. 6 fma-pipe cycles per
+                # warp-evaluation instead of the 7 `peak` assumes
+                "frac_of_6_cycle_screen_bound": (achieved / k1_peak(evals, f_max, screened=32.0 / 6.0)) if achieved else None,
                 "evals_per_launch": evals[0], "evals_exact_kernel": evals[1], "evals_screened_kernel": evals[2],
                 "ms_per_launch": k1_per_launch_ms,
                 "share_of_step": (k1_ms / max(1, args.steps)) / (ms / args.steps)}
