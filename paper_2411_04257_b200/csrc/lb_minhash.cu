@@ -1029,21 +1029,7 @@ template <int NPL, int PASSES, int MINB = 2, bool GATED = false, int G = 4, int 
 __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const MinhashParams p) {
   static_assert(R == 1 || (R == 2 && G == 8), "deferred resolution packs two chunks' 4 groups");
   __shared__ XLimbs xs[R][K1_WARPS][32];     // exact-evaluation limbs (R chunks)
-#ifdef LB_SCR4_FFMA2
-  __shared__ uint2 xfi[R][K1_WARPS][32];     // screen limbs {xl, xh}
-  __shared__ float4 xf2[R][K1_WARPS][32];    // {XL, XL, XH, XH}: broadcast pairs for the packed FMA
-  struct XfView {                            // xf[bf][w][i] as an XLimbsS
-    const uint2 (*a)[K1_WARPS][32]; const float4 (*b)[K1_WARPS][32];
-    struct L2 { const uint2* a; const float4* b;
-      __device__ __forceinline__ XLimbsS operator[](uint32_t i) const { XLimbsS f; f.xl = a[i].x; f.xh = a[i].y; f.XL = b[i].x; f.XH = b[i].z; return f; } };
-    struct L1 { const uint2 (*a)[32]; const float4 (*b)[32];
-      __device__ __forceinline__ L2 operator[](uint32_t i) const { return L2{a[i], b[i]}; } };
-    __device__ __forceinline__ L1 operator[](uint32_t i) const { return L1{a[i], b[i]}; }
-  };
-  const XfView xf{xfi, xf2};
-#else
   __shared__ XLimbsS xf[R][K1_WARPS][32];    // screen limbs
-#endif
   __shared__ uint32_t sg[K1_WARPS][32 * NPL * PASSES];
   __shared__ uint32_t kq[K1_WARPS][NPL][32];  // thresholds while flagged groups are resolved
   constexpr uint32_t kRQ = 512;                 // balanced-resolution queue per warp (the rest per lane)
@@ -1135,12 +1121,7 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
           f.xh = (uint32_t)(x >> 32);
           f.XL = __uint2float_rn(f.xl) * 0x1p-29f;
           f.XH = __uint2float_rn(f.xh) * 0x1p-29f;
-#ifdef LB_SCR4_FFMA2
-          xfi[bf][w][lane] = make_uint2(f.xl, f.xh);
-          xf2[bf][w][lane] = make_float4(f.XL, f.XL, f.XH, f.XH);
-#else
           xf[bf][w][lane] = f;
-#endif
         }
         __syncwarp();
         const uint32_t cnt = min(32u, S - s0);
@@ -1181,40 +1162,6 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
             const uint32_t gb[4] = {gb0, gb0 << 8, gb0 << 16, gb0 << 24};
 #pragma unroll
             for (int u = 0; u < G; u++) xv[u] = xf[bf][w][j + u];
-#ifdef LB_SCR4_FFMA2
-            // two permutation slots per packed FMA (fma.rn.f32x2): half the FFMA issue slots
-            ulonglong2 x2[G];
-#pragma unroll
-            for (int u = 0; u < G; u++) x2[u] = *reinterpret_cast<const ulonglong2*>(&xf2[bf][w][j + u]);
-#pragma unroll
-            for (int qp = 0; qp < NPL / 2; qp++) {
-              uint32_t mn[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
-              unsigned long long ALp, AHp;
-              asm("mov.b64 %0, {%1, %2};" : "=l"(ALp) : "f"(AL[2 * qp]), "f"(AL[2 * qp + 1]));
-              asm("mov.b64 %0, {%1, %2};" : "=l"(AHp) : "f"(AH[2 * qp]), "f"(AH[2 * qp + 1]));
-#pragma unroll
-              for (int u = 0; u < G; u++) {
-                unsigned long long d1, d2;
-                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d1) : "l"(ALp), "l"(x2[u].y), "l"(0x50C0000050C00000ull));
-                asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d2) : "l"(AHp), "l"(x2[u].x), "l"(d1));
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                  const int q = 2 * qp + h;
-                  uint32_t t, hb;
-                  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(al[q]), "r"(xv[u].xl), "r"(lb[q]));
-                  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(a8h[q]), "r"(xv[u].xh), "r"(t));
-                  asm("shf.l.wrap.b32 %0, %1, %2, 11;" : "=r"(hb) : "r"(0u), "r"((uint32_t)(h ? d2 >> 32 : d2)));
-                  mn[h] = min(mn[h], t + hb);
-                }
-              }
-#pragma unroll
-              for (int h = 0; h < 2; h++) {
-                const int q = 2 * qp + h;
-                if (q < 4) asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(cml) : "r"(mn[h]), "r"(K[q]), "r"(gb[q & 3]));
-                else asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(cmh) : "r"(mn[h]), "r"(K[q]), "r"(gb[q & 3]));
-              }
-            }
-#else
 #pragma unroll
             for (int q = 0; q < NPL; q++) {
               uint32_t mn = 0xFFFFFFFFu;
@@ -1223,7 +1170,6 @@ __global__ void __launch_bounds__(K1_THREADS, MINB) k1_minhash_scr4(const Minhas
               if (q < 4) asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(cml) : "r"(mn), "r"(K[q]), "r"(gb[q & 3]));
               else asm("{ .reg .pred p; setp.lt.u32 p, %1, %2; @p or.b32 %0, %0, %3; }" : "+r"(cmh) : "r"(mn), "r"(K[q]), "r"(gb[q & 3]));
             }
-#endif
           }
           cm |= ((uint64_t)cmh << 32) | cml;
           // the chunk's last (cnt - j0) mod G shingles: exactly (warp-uniform)
