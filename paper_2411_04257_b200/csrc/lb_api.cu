@@ -107,7 +107,7 @@ struct lshbloom {
     // when the batch's last K1 launch is done (the next copy into this buffer waits for it)
     DevBuf tokall;
     uint32_t* landed = nullptr;
-    cudaEvent_t tok_free = nullptr;
+    cudaEvent_t tok_free = nullptr, land_zero = nullptr;   // land_zero: this batch's counter zeroed (copy stream)
   } slot[2];
   int next_slot = 0;
   uint64_t seq = 0;
@@ -197,6 +197,7 @@ void free_all(lshbloom* h) {
     F(sl.bh.p); F(sl.off.p); F(sl.dup.p); F(sl.tokall.p); F(sl.landed);
     if (sl.done) cudaEventDestroy(sl.done);
     if (sl.tok_free) cudaEventDestroy(sl.tok_free);
+    if (sl.land_zero) cudaEventDestroy(sl.land_zero);
   }
   if (h->k1_stream1) cudaStreamDestroy(h->k1_stream1);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
@@ -945,7 +946,6 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
     p.offsets = (const uint64_t*)sl.off.p;
     if (landing) {
       LB_CUDA(h, ensure(sl.tokall, n_tok_host * sizeof(uint32_t)));   // (the slot is idle: collected)
-      LB_CUDA(h, cudaMemsetAsync(sl.landed, 0, 4, s0));
       p.tokens = (const uint32_t*)sl.tokall.p;
       p.tok_base = 0;
       p.landed = sl.landed;
@@ -965,10 +965,17 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
   LB_CUDA(h, cudaEventRecord(h->ev_pre, s0));               // error gate and offsets ready
   if (landing) {
     // every piece and its landing mark are enqueued before any K1 launch, so a waiting warp
-    // only ever waits on copy-engine work (no SM involved); the copies start once the slot's
-    // previous K1 reader is done and this batch's landing counter is zeroed
-    LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_pre, 0));
+    // only ever waits on copy-engine work (no SM involved).  The copies depend only on the
+    // caller's inputs and on the slot's previous K1 reader -- not on the K1 streams' position --
+    // so with two slots batch t+1's tokens land while batch t's K1 still runs (the copy engine
+    // never idles between streamed host batches); the landing counter is zeroed on the copy
+    // stream itself, and the K1 streams wait for that (a stale count would open the gate early)
+    LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_in, 0));
     LB_CUDA(h, cudaStreamWaitEvent(h->copy_stream, sl.tok_free, 0));
+    // (a stream write, not a memset: a memset kernel would queue behind the resident K1 blocks)
+    if (h->write_value32((CUstream)h->copy_stream, (CUdeviceptr)sl.landed, 0u, 0) != CUDA_SUCCESS)
+      return fail(h, LSHBLOOM_ERUNTIME, "cuStreamWriteValue32 failed");
+    LB_CUDA(h, cudaEventRecord(sl.land_zero, h->copy_stream));
     const uint64_t piece = 1ull << h->land_log2;
     uint32_t i = 0;
     for (uint64_t t0 = 0; t0 < n_tok_host; t0 += piece) {
@@ -985,6 +992,8 @@ int run_query_insert(lshbloom* h, const lshbloom_batch* b, cudaStream_t s, int s
     }
   }
   for (int k = 1; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], h->ev_pre, 0));
+  if (landing)
+    for (int k = 0; k < nks; k++) LB_CUDA(h, cudaStreamWaitEvent(kst[k], sl.land_zero, 0));
   LB_CUDA(h, cudaStreamWaitEvent(h->bloom_stream, h->ev_pre, 0));
   LB_CUDA(h, cudaMemsetAsync(ddup, 0, n, h->bloom_stream));
   int c = 0;
@@ -1190,6 +1199,7 @@ int lshbloom_create_ex(const lshbloom_config* cfg, lshbloom** out) {
   for (auto& sl : h->slot) {
     CR(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
     CR(cudaEventCreateWithFlags(&sl.tok_free, cudaEventDisableTiming));
+    CR(cudaEventCreateWithFlags(&sl.land_zero, cudaEventDisableTiming));
     CR(cudaMalloc(&sl.landed, 4));
     CR(cudaMemset(sl.landed, 0, 4));
   }
