@@ -120,3 +120,25 @@ def test_async_c3_sweep_stream():
     idx.sync()
     assert (np.concatenate([u8(x) for x in outs]) == dup).all()
     assert idx.info()["sweeps"] == 4
+
+
+def test_async_c3_host_stream_varying_sizes():
+    # landing-gated host batches of very different sizes in a row (3-4 landing pieces, then one,
+    # ...): each slot's landing counter restarts from zero on the copy stream before the batch's
+    # K1 may read it, and batch t+1's copy runs while batch t's K1 does (Overlap)
+    cfg = CONFIGS["C3"]
+    off, tok = gen_range(cfg, 0, 4000)
+    _, _, dup, _ = oracle.run(off, tok, num_perm=cfg.num_perm, b=cfg.b, r=cfg.r, n_expected=cfg.n_docs,
+                              fp_rate=cfg.fp_rate, seed=cfg.seed)
+    idx = LSHBloom(cfg.num_perm, cfg.b, cfg.r, cfg.n_docs, cfg.fp_rate, cfg.seed, device=0)
+    outs, keep = [], []
+    for o, t in pieces(off, tok, [0, 1500, 1600, 3200, 3300, 3301, 4000]):
+        o = torch.from_numpy(o.view(np.int64)).pin_memory()
+        t = torch.from_numpy(t.view(np.int32)).pin_memory()
+        out = torch.empty(len(o) - 1, dtype=torch.uint8).pin_memory()
+        keep.append((o, t))
+        outs.append(idx.query_insert_async(o, t, out=out))
+    idx.sync()
+    got = np.concatenate([u8(x) for x in outs])
+    assert (got == dup).all(), np.flatnonzero(got != dup)[:10]
+    assert dup.sum() > 0 and idx.info()["doc_count"] == 4000
